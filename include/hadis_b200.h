@@ -1,0 +1,180 @@
+/*
+ * hadis_b200.h -- C ABI of libhadis_b200.so, the B200 (sm_100a) implementation
+ * of HADIS's offline cascade-profiling + runtime-allocation hot path.
+ *
+ * The reference (cascadesim 0.1.0, pure Python + numpy) has no native code and
+ * no FFI; its Python entry points are the contract.  Each function below is
+ * the device-side replacement of one stage of those entry points and cites the
+ * reference code it replaces (paths relative to /root/reference/pkg/src/cascadesim).
+ * INTEGRATION.md shows the ctypes binding cascadesim would add.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers owned by the caller (allocate with
+ *     cudaMalloc, torch, cupy ...).  Nothing here allocates device memory except
+ *     out of a caller-provided workspace.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every call only enqueues work; nothing synchronises the host.
+ *   - Return value: 0 (HADIS_OK) or a hadis_status code.  Data-dependent
+ *     failures that can only be known on the device (bad records, capacity
+ *     overflow) are reported through the `stats` arrays documented per call.
+ *   - float64 arithmetic that must match the reference bit for bit is compiled
+ *     without FMA contraction (-fmad=false + __d*_rn intrinsics).
+ */
+#ifndef HADIS_B200_H
+#define HADIS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HADIS_ABI_VERSION 1
+
+enum hadis_status {
+  HADIS_OK = 0,
+  HADIS_ERR_ARG = 1,          /* invalid argument (sizes, null pointers)          */
+  HADIS_ERR_RECORDS = 2,      /* hardness not finite or outside [0, 1]            */
+  HADIS_ERR_CAPACITY = 3,     /* caller buffer / workspace too small              */
+  HADIS_ERR_CUDA = 4,         /* CUDA runtime error (hadis_last_cuda_error)       */
+  HADIS_ERR_NO_ROWS = 5,      /* planner: "fallback: no serveable rows"           */
+  HADIS_ERR_NEG_DEMAND = 6,   /* planner: "solve: negative demand"                */
+  HADIS_ERR_UNSUPPORTED = 7   /* outside the implemented envelope */
+};
+
+int hadis_abi_version(void);
+const char* hadis_status_string(int status);
+const char* hadis_last_cuda_error(void);
+
+/* ------------------------------------------------------------------------- */
+/* Profiling: grid evaluator + Pareto extractor                               */
+/* replaces profiler.profile_config's numeric core (profiler.py:133-174) and   */
+/* catalog.pareto_prune as it is used there (catalog.py:171-192).              */
+/* ------------------------------------------------------------------------- */
+
+/* Fixed-point scale for hardness sums: h_fix = floor(h * 2^shift), with
+ * shift = 63 - bit_length(n) so that every sum of n values fits in 63 bits. */
+int hadis_hfix_shift(int64_t n);
+
+/* K1 -- bin + 2-D histogram (profiler.py:138, 145-150: bypass h > theta,
+ * reject score < tau).  For every record q and light model l:
+ *   bh = #{u < h[q]},  bs = #{u <= s_l[q]}   (u = sorted distinct thresholds)
+ *   hist_cnt [l][bh][bs] += 1 ;  hist_hsum[l][bh][bs] += floor(h[q] * 2^shift)
+ * scores: n_light rows of n float64 (row stride n).  Histograms have
+ * (n_unique+1)^2 cells per light model and are zeroed by this call.
+ * bad_records (device uint32) counts records with h outside [0, 1] / NaN. */
+int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_light,
+                   const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
+                   uint32_t* hist_cnt, uint64_t* hist_hsum, uint32_t* bad_records,
+                   void* stream);
+
+/* K2 -- in-place 2-D inclusive prefix sums of the K1 histograms:
+ *   cnt[l][k][t] = #{q : bh(q) <= k, bs_l(q) <= t}  (and the same for hsum). */
+int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t n_light,
+                    int32_t n_unique, void* stream);
+
+/* Per-pair parameters, row-major [n_pairs][HADIS_PAIR_PARAMS] doubles:
+ * {latency_s[1] light, latency_s[1] heavy, base cost light, penalty light,
+ *  base cost heavy, penalty heavy}. */
+#define HADIS_PAIR_PARAMS 6
+
+/* Layout of the `stats` int64 array written by hadis_pair_frontiers. */
+enum hadis_frontier_stat {
+  HADIS_ST_ROWS = 0,        /* total output rows                                  */
+  HADIS_ST_CANDIDATES = 1,  /* main-universe candidates that passed the filter    */
+  HADIS_ST_UNCERTAIN = 2,   /* decisions resolved with the exact numpy emulation  */
+  HADIS_ST_EXACT_CELLS = 3, /* cells whose fidelity was recomputed exactly        */
+  HADIS_ST_OVERFLOW = 4,    /* nonzero: a capacity was exceeded, rerun bigger     */
+  HADIS_ST_PAIR0 = 8        /* then n_pairs per-pair output row counts            */
+};
+
+size_t hadis_frontier_workspace_bytes(int32_t n_pairs, int32_t n_unique, int64_t cand_cap,
+                                      int64_t exact_cap, int64_t out_cap);
+
+/* K3 + K4 -- per pair (light slot, heavy): evaluate every (theta, tau) cell
+ * from the K2 prefix tables, extract the latency/fidelity Pareto frontier and
+ * the theta = max(thresholds) no-bypass frontier, merge them and emit the rows
+ * sorted by (theta, tau) -- profiler.py:140-174.  Decisions are exact: cells
+ * whose order against another cell cannot be certified from the fixed-point
+ * fidelity bound are recomputed with a bit-exact emulation of numpy's
+ * pairwise mean over (h, scores) and decided on those values.
+ *
+ *   pre_cnt / pre_hsum : K2 output, slots indexed by pair_slot[p]
+ *   pair_slot[p]       : light-model slot (row of `scores`, K1/K2 slot)
+ *   pair_params        : [n_pairs][HADIS_PAIR_PARAMS]
+ *   first_pos[r]       : smallest position in the caller's threshold list of
+ *                        the r-th smallest distinct threshold value
+ *   n_thresholds       : length of the caller's threshold list (K)
+ *   exact_fid          : nonzero = recompute the fidelity of every OUTPUT row
+ *                        with the numpy emulation (bit-identical rows)
+ *   outputs (capacity out_cap rows, pair-major, (theta, tau) order):
+ *     out_pair, out_theta_pos, out_tau_pos (positions in the caller's list),
+ *     out_r_light, out_r_heavy, out_fid, out_lat
+ *   stats              : int64[HADIS_ST_PAIR0 + n_pairs], see hadis_frontier_stat */
+int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
+                         int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
+                         const int32_t* pair_slot, const double* pair_params,
+                         const int32_t* first_pos, int32_t n_thresholds,
+                         const double* thr_unique, const double* h, const double* scores,
+                         int32_t exact_fid, void* workspace, size_t workspace_bytes,
+                         int64_t cand_cap, int64_t exact_cap, int64_t out_cap,
+                         int32_t* out_pair, int32_t* out_theta_pos, int32_t* out_tau_pos,
+                         double* out_r_light, double* out_r_heavy, double* out_fid,
+                         double* out_lat, int64_t* stats, void* stream);
+
+/* numpy-exact mean of where(h > theta | s < tau, cost_heavy, cost_light)
+ * (profiler.py:152-153) for n_cells cells: cell c uses score row
+ * cell_slot[c], thresholds cell_theta[c] / cell_tau[c] and cost parameters
+ * cell_params[c] = {base_l, pen_l, base_h, pen_h}.  out_fid[c] is bitwise
+ * equal to float(np.where(...).mean()) on the same float64 inputs. */
+int hadis_fid_exact(const double* h, const double* scores, int64_t n, int32_t n_cells,
+                    const int32_t* cell_slot, const double* cell_theta, const double* cell_tau,
+                    const double* cell_params, double* out_fid, void* stream);
+
+/* Generic pareto_prune (catalog.py:171-192) over n (latency, quality) keys:
+ * out_idx receives the kept original indices in the reference's output order
+ * ((latency, quality, index) ascending); out_count[0] their number.
+ * NaN keys are rejected with HADIS_ERR_ARG by the host wrapper. */
+size_t hadis_pareto_workspace_bytes(int64_t n);
+int hadis_pareto_prune(const double* lat, const double* qual, int64_t n, int64_t* out_idx,
+                       int64_t* out_count, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Allocation search: planner.solve over many (demand, SLO) points           */
+/* replaces _solve_over_rows / _evaluate_row / fallback_plan                  */
+/* (planner.py:81-227).                                                       */
+/* ------------------------------------------------------------------------- */
+
+/* Rows: row_model[r][2] = {light model, heavy model} (indices into the model
+ * tables; equal for single-model rows), row_share[r][2] = {r_light, r_heavy},
+ * row_fid[r] = fidelity_cost.  Models: lat[m][n_batch], mu[m][n_batch]
+ * (latency_s / throughput_qps in catalog.batch_sizes order), lat1[m] =
+ * latency_s[1].  batch_sizes[n_batch].  Points: lam[p], t_slo[p],
+ * workers[p], queues[p][n_models] (0 = no backlog), alpha (shared).
+ *
+ * Per point the result is written to:
+ *   plan_row[p]      chosen row index (-1 = no serveable rows -> PlannerError)
+ *   plan_x[p][2]     worker counts {light, heavy} (heavy unused for 1-model rows)
+ *   plan_b[p][2]     batch sizes   {light, heavy}
+ *   plan_path[p]     path latency (bit-exact with the reference)
+ *   plan_flags[p]    bit0 = infeasible (fallback plan), bit1 = negative demand
+ * Ties are broken exactly as the reference: per row min (total, path) first
+ * combo wins; globally min (fidelity, total, path, row index); fallback max
+ * capacity then (latency_s[1] light, latency_s[1] heavy, row index). */
+size_t hadis_solve_workspace_bytes(int32_t n_points, int32_t n_rows);
+int hadis_solve_many(int32_t n_rows, const int32_t* row_model, const double* row_share,
+                     const double* row_fid, int32_t n_models, int32_t n_batch,
+                     const int32_t* batch_sizes, const double* lat, const double* mu,
+                     const double* lat1, int32_t n_points, const double* lam,
+                     const double* t_slo, const int32_t* workers, const double* queues,
+                     double alpha, int32_t* plan_row, int32_t* plan_x, int32_t* plan_b,
+                     double* plan_path, int32_t* plan_flags, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HADIS_B200_H */

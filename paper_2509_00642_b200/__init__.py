@@ -1,0 +1,18 @@
+"""B200-native HADIS cascade profiling + allocation search (arxiv 2509.00642).
+
+Drop-in for the hot path of the reference package ``cascadesim`` 0.1.0:
+``profiler.profile_config`` (grid evaluator + Pareto extractor),
+``catalog.pareto_prune`` and ``planner.solve`` (allocation search).  The
+compute runs in ``libhadis_b200.so`` (hand-written sm_100a CUDA, C ABI in
+``include/hadis_b200.h``); this package is the host-side mirror of the
+reference's Python interface for that path.
+"""
+
+__version__ = "0.1.0"
+
+from .catalog import (Catalog, CatalogError, ModelVariant, default_catalog,  # noqa: F401
+                      make_variant, pareto_prune, scaled_batch_profile, select_candidates)
+from .planner import Plan, PlannerError, fallback_plan, solve, solve_many  # noqa: F401
+from .profiler import (THRESHOLD_GRID, CascadeRow, CascadeTable, GridProfiler,  # noqa: F401
+                       ProfileError, TableProvenance, load_table, profile_config,
+                       profile_records, prompts_hash, save_table)

@@ -1,0 +1,28 @@
+// ABI housekeeping: version, status strings, last CUDA error.
+#include <cstring>
+
+#include "common.cuh"
+
+static thread_local char g_last_cuda_error[256] = "";
+
+void hadis_set_cuda_error(cudaError_t e) {
+  std::strncpy(g_last_cuda_error, cudaGetErrorString(e), sizeof(g_last_cuda_error) - 1);
+}
+
+extern "C" int hadis_abi_version(void) { return HADIS_ABI_VERSION; }
+
+extern "C" const char* hadis_last_cuda_error(void) { return g_last_cuda_error; }
+
+extern "C" const char* hadis_status_string(int status) {
+  switch (status) {
+    case HADIS_OK: return "ok";
+    case HADIS_ERR_ARG: return "invalid argument";
+    case HADIS_ERR_RECORDS: return "records: hardness must be finite and within [0, 1]";
+    case HADIS_ERR_CAPACITY: return "capacity exceeded";
+    case HADIS_ERR_CUDA: return "cuda error";
+    case HADIS_ERR_NO_ROWS: return "fallback: no serveable rows";
+    case HADIS_ERR_NEG_DEMAND: return "solve: negative demand";
+    case HADIS_ERR_UNSUPPORTED: return "unsupported configuration";
+    default: return "unknown status";
+  }
+}

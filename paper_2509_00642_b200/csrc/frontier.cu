@@ -1,0 +1,1014 @@
+// K3 + K4: grid-cell evaluation, Pareto extraction and row emission.
+//
+// Reference: pkg/src/cascadesim/profiler.py:140-174 and catalog.py:171-192.
+// For each pair (light i, heavy j) and each distinct-threshold cell (k, t):
+//   nb = n - R[k]            (R[k] = #{bh <= k}: records not bypassed)
+//   nr = C_i[k][t]           (non-bypassed and s_i < tau)
+//   lat = ((n-nb)*L_i + (nb+nr)*L_j) / n          -- bit-exact, no FMA
+//   r_light = (n-nb)/n, r_heavy = (nb+nr)/n          -- bit-exact
+//   fid* = (b_j*nH + b_i*nL + (p_j*SH + p_i*SL)*2^-shift) / n
+// where SH/SL are exact fixed-point hardness sums.  fid* differs from numpy's
+// pairwise mean by at most delta (a rigorous per-pair bound), so a Pareto
+// decision is "certain" unless two cells' fid* lie within 2*delta and their
+// heavy sets differ (equal heavy sets give bitwise-equal fidelities in both
+// numpy and here).  Uncertain decisions are re-decided on numpy-exact values
+// from the pairwise emulation (pairwise.cuh).
+//
+// Pipeline (all stream-ordered, no host synchronisation):
+//   F1 bucket minima   per pair, latency buckets -> min fid*          (atomicMin)
+//   F2 prefix minima   exclusive prefix-min over buckets
+//   F3 filter          keep cells with fid* <= prefix-min + 2 delta (candidates)
+//   F4/F5 group        counting sort of candidates by (pair, bucket)
+//   F6 decide          kill / keep / uncertain per candidate (in-bucket compare,
+//                      heavy-set twin test, prefix-min margin)
+//   F7 no-bypass row   theta = max(thresholds) sub-frontier (profiler.py:168-170)
+//   F8-F11             partners of uncertain cells -> numpy-exact fid -> decide
+//   F12 emit           kept-cell bitmap -> rows in (theta, tau) order
+//   F13/F14            exact fidelity patch for emitted rows
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "pairwise.cuh"
+
+namespace hadis {
+
+enum : uint32_t { kKept = 1u, kUncertain = 2u };
+
+struct PairConst {
+  double Ll, Lh, bl, pl, bh, ph;
+  double delta2;     // 2 * delta
+  double lo, scale;  // latency bucket map
+  int slot;
+};
+
+struct Grid {
+  const uint32_t* cnt;      // K2 prefix counts [slot][B1][B1]
+  const uint64_t* hs;       // K2 prefix hardness sums
+  int64_t n;
+  int U, B1;
+  double inv_scale;         // 2^-shift
+  int nbuckets;
+  int K;
+  const int32_t* first_pos;
+  int64_t bm_stride;        // bits per pair in the kept bitmap (words_per_pair * 32)
+};
+
+struct CellVal {
+  double lat, fid;
+  uint32_t n_keep_light;    // R[k]  (= n - nb)
+  uint32_t n_heavy;         // nb + nr
+};
+
+__device__ __forceinline__ const uint32_t* slot_cnt(const Grid& g, int slot) {
+  return g.cnt + (int64_t)slot * g.B1 * g.B1;
+}
+__device__ __forceinline__ const uint64_t* slot_hs(const Grid& g, int slot) {
+  return g.hs + (int64_t)slot * g.B1 * g.B1;
+}
+
+__device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc, int k, int t) {
+  const uint32_t* C = slot_cnt(g, pc.slot);
+  const uint64_t* S = slot_hs(g, pc.slot);
+  const int64_t rk = (int64_t)k * g.B1;
+  const uint32_t Rk = C[rk + g.U];
+  const uint64_t Rhk = S[rk + g.U];
+  const uint64_t Htot = S[(int64_t)g.U * g.B1 + g.U];
+  const uint32_t nr = C[rk + t];
+  const uint64_t sh_rej = S[rk + t];
+  const uint32_t n = (uint32_t)g.n;
+  const uint32_t nH = (n - Rk) + nr;
+  const uint64_t SH = (Htot - Rhk) + sh_rej;
+  const uint64_t SL = Htot - SH;
+  CellVal v;
+  v.n_keep_light = Rk;
+  v.n_heavy = nH;
+  const double dn = (double)g.n;
+  v.lat = __ddiv_rn(__dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh)), dn);
+  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)SH), __dmul_rn(pc.pl, (double)SL)),
+                                 g.inv_scale);
+  const double base = __dadd_rn(__dmul_rn(pc.bh, (double)nH), __dmul_rn(pc.bl, (double)(n - nH)));
+  v.fid = __ddiv_rn(__dadd_rn(base, hterm), dn);
+  return v;
+}
+
+__device__ __forceinline__ int bucket_of(const PairConst& pc, int nbuckets, double lat) {
+  double x = floor(__dmul_rn(__dadd_rn(lat, -pc.lo), pc.scale));
+  if (!(x >= 0.0)) x = 0.0;
+  if (x > (double)(nbuckets - 1)) x = (double)(nbuckets - 1);
+  return (int)x;
+}
+
+__device__ __forceinline__ int64_t grid_index(const Grid& g, int k, int t) {
+  return (int64_t)g.first_pos[k] * g.K + g.first_pos[t];
+}
+
+// equal heavy sets H(k1,t1) == H(k2,t2) from prefix counts (exact)
+__device__ bool same_heavy(const Grid& g, int slot, int k1, int t1, int k2, int t2) {
+  if (k1 > k2) { int x = k1; k1 = k2; k2 = x; x = t1; t1 = t2; t2 = x; }
+  const uint32_t* C = slot_cnt(g, slot);
+  const uint32_t n = (uint32_t)g.n;
+  const int64_t r1 = (int64_t)k1 * g.B1, r2 = (int64_t)k2 * g.B1;
+  const uint32_t h1 = (n - C[r1 + g.U]) + C[r1 + t1];
+  const uint32_t h2 = (n - C[r2 + g.U]) + C[r2 + t2];
+  if (h1 != h2) return false;
+  const int tm = t1 < t2 ? t1 : t2;
+  const uint32_t inter = (n - C[r2 + g.U]) + (C[r2 + t2] - C[r1 + t2]) + C[r1 + tm];
+  return inter == h1;
+}
+
+// ---------------------------------------------------------------- F0: setup
+
+__global__ void pair_const_kernel(int n_pairs, const int32_t* __restrict__ pair_slot,
+                                  const double* __restrict__ params, int64_t n, int shift,
+                                  int nbuckets, PairConst* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const double* q = params + (int64_t)p * HADIS_PAIR_PARAMS;
+  PairConst c;
+  c.Ll = q[0]; c.Lh = q[1]; c.bl = q[2]; c.pl = q[3]; c.bh = q[4]; c.ph = q[5];
+  c.slot = pair_slot[p];
+  // |numpy pairwise mean - fid*| <= (D + 16) u Fmax + maxpen * n * 2^-shift / n,
+  // D <= 96 covers numpy's recursion for any n < 2^64; doubled for margin.
+  const double u = ldexp(1.0, -53);
+  const double fbig = fmax(fabs(c.bl) + fabs(c.pl), fabs(c.bh) + fabs(c.ph));
+  const double pmax = fmax(fabs(c.pl), fabs(c.ph));
+  const double delta = 2.0 * (128.0 * u * fbig + pmax * ldexp(1.0, -shift)) + DBL_MIN;
+  c.delta2 = 2.0 * delta;
+  const double lo = fmin(c.Ll, c.Lh) * (1.0 - 1e-12);
+  const double hi = (c.Ll + c.Lh) * (1.0 + 1e-12);
+  c.lo = lo;
+  c.scale = (double)nbuckets / (hi - lo);
+  (void)n;
+  out[p] = c;
+}
+
+// pk[k] = largest k' < k with R[k'] < R[k] (else -1): canonical heavy-set twin row
+__global__ void twin_row_kernel(const uint32_t* __restrict__ cnt, int U, int B1, int32_t* pk) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int last = -1;         // last rank whose R differs from the run that follows
+  uint32_t prevR = 0;
+  for (int k = 0; k < U; ++k) {
+    const uint32_t Rk = cnt[(int64_t)k * B1 + U];
+    if (k > 0 && Rk != prevR) last = k - 1;
+    pk[k] = last;
+    prevR = Rk;
+  }
+}
+
+// ---------------------------------------------------------- F1: bucket minima
+
+constexpr int kCellThreads = 256;
+
+__global__ void __launch_bounds__(kCellThreads)
+bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
+                  unsigned long long* __restrict__ bmin) {
+  const int64_t cells = (int64_t)g.U * g.U;
+  const int64_t total = cells * n_pairs;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int p = (int)(i / cells);
+    const int64_t c = i - (int64_t)p * cells;
+    const int k = (int)(c / g.U), t = (int)(c % g.U);
+    const PairConst pc = pcs[p];
+    const CellVal v = eval_cell(g, pc, k, t);
+    const int b = bucket_of(pc, g.nbuckets, v.lat);
+    atomicMin(&bmin[(int64_t)p * g.nbuckets + b], (unsigned long long)order_key(v.fid));
+  }
+}
+
+// ------------------------------------------------- F2: exclusive prefix minima
+
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads)
+bucket_prefix_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
+                     double* __restrict__ gpre) {
+  __shared__ unsigned long long part[kScanThreads];
+  const int p = blockIdx.x;
+  const unsigned long long* src = bmin + (int64_t)p * nbuckets;
+  double* dst = gpre + (int64_t)p * nbuckets;
+  const int per = (nbuckets + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per;
+  const int hi = min(nbuckets, lo + per);
+  unsigned long long m = ~0ull;
+  for (int i = lo; i < hi; ++i) m = min(m, src[i]);
+  part[threadIdx.x] = m;
+  __syncthreads();
+  // Hillis-Steele inclusive min-scan over the per-thread minima
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : ~0ull;
+    __syncthreads();
+    part[threadIdx.x] = min(part[threadIdx.x], o);
+    __syncthreads();
+  }
+  unsigned long long run = threadIdx.x > 0 ? part[threadIdx.x - 1] : ~0ull;
+  for (int i = lo; i < hi; ++i) {
+    dst[i] = run == ~0ull ? INFINITY : from_order_key(run);
+    run = min(run, src[i]);
+  }
+}
+
+// ------------------------------------------------------------- F3: filter
+
+struct Cands {
+  uint32_t* pair;
+  uint32_t* cell;     // k * U + t
+  uint32_t* bucket;
+  double* lat;
+  double* fid;
+};
+
+__global__ void __launch_bounds__(kCellThreads)
+filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
+              const double* __restrict__ gpre, uint32_t* __restrict__ bcnt, Cands raw,
+              int64_t cap, unsigned long long* __restrict__ counters) {
+  const int64_t cells = (int64_t)g.U * g.U;
+  const int64_t total = cells * n_pairs;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool take = false;
+    int p = 0, b = 0, k = 0, t = 0;
+    CellVal v{};
+    if (i < total) {
+      p = (int)(i / cells);
+      const int64_t c = i - (int64_t)p * cells;
+      k = (int)(c / g.U);
+      t = (int)(c % g.U);
+      const PairConst pc = pcs[p];
+      v = eval_cell(g, pc, k, t);
+      b = bucket_of(pc, g.nbuckets, v.lat);
+      take = v.fid <= gpre[(int64_t)p * g.nbuckets + b] + pc.delta2;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (!mask) continue;
+    unsigned long long slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(&counters[0], (unsigned long long)__popc(mask));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (take) {
+      const int64_t at = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
+      atomicAdd(&bcnt[(int64_t)p * g.nbuckets + b], 1u);
+      if (at < cap) {
+        raw.pair[at] = (uint32_t)p;
+        raw.cell[at] = (uint32_t)(k * g.U + t);
+        raw.bucket[at] = (uint32_t)b;
+        raw.lat[at] = v.lat;
+        raw.fid[at] = v.fid;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------- F4: offsets (exclusive scan)
+
+// one block: exclusive scan of n u32 values into u64 offsets (n = pairs * buckets)
+__global__ void __launch_bounds__(kScanThreads)
+exclusive_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
+                      unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long part[kScanThreads];
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = threadIdx.x * per;
+  const int64_t hi = lo + per < n ? lo + per : n;
+  unsigned long long s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += in[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : 0ull;
+    __syncthreads();
+    part[threadIdx.x] += o;
+    __syncthreads();
+  }
+  unsigned long long run = threadIdx.x > 0 ? part[threadIdx.x - 1] : 0ull;
+  for (int64_t i = lo; i < hi; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) out[n] = part[blockDim.x - 1];
+}
+
+// ------------------------------------------------------------ F5: scatter
+
+__global__ void scatter_kernel(Cands raw, const unsigned long long* __restrict__ counters,
+                               int64_t cap, int nbuckets,
+                               const unsigned long long* __restrict__ boff,
+                               uint32_t* __restrict__ bcur, Cands grp) {
+  if ((int64_t)counters[0] > cap) return;   // overflow: host reruns with more room
+  const int64_t m = (int64_t)counters[0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int64_t key = (int64_t)raw.pair[i] * nbuckets + raw.bucket[i];
+    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
+    if (at >= cap) continue;
+    grp.pair[at] = raw.pair[i];
+    grp.cell[at] = raw.cell[i];
+    grp.bucket[at] = raw.bucket[i];
+    grp.lat[at] = raw.lat[i];
+    grp.fid[at] = raw.fid[i];
+  }
+}
+
+// --------------------------------------------------------------- F6: decide
+
+struct Uncertain {
+  uint32_t* universe;
+  uint32_t* pair;
+  uint32_t* cell;
+};
+
+__device__ __forceinline__ void set_bit(uint32_t* bm, int64_t bit) {
+  atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+}
+__device__ __forceinline__ bool get_bit(const uint32_t* bm, int64_t bit) {
+  return (bm[bit >> 5] >> (bit & 31)) & 1u;
+}
+
+// Request numpy-exact fidelity for a cell (deduplicated through a bitmap).
+__device__ void request_exact(int64_t cells, int p, uint32_t cell, uint32_t* req_bm,
+                              uint32_t* req_pair, uint32_t* req_cell, int64_t cap,
+                              unsigned long long* counters) {
+  const int64_t bit = (int64_t)p * cells + cell;
+  const uint32_t m = 1u << (bit & 31);
+  const uint32_t old = atomicOr(&req_bm[bit >> 5], m);
+  if (old & m) return;
+  const unsigned long long at = atomicAdd(&counters[2], 1ull);
+  if ((int64_t)at < cap) { req_pair[at] = (uint32_t)p; req_cell[at] = cell; }
+}
+
+__device__ void push_uncertain(int universe, int p, uint32_t cell, Uncertain un, int64_t cap,
+                               unsigned long long* counters) {
+  const unsigned long long at = atomicAdd(&counters[1], 1ull);
+  if ((int64_t)at < cap) { un.universe[at] = universe; un.pair[at] = p; un.cell[at] = cell; }
+}
+
+// kill(d, c) for d with lat_d <= lat_c, given fidelities known to be comparable
+__device__ __forceinline__ bool kills(double fd, double fc, double lat_d, double lat_c,
+                                      int64_t idx_d, int64_t idx_c) {
+  return fd < fc || (fd == fc && (lat_d < lat_c || idx_d < idx_c));
+}
+
+__global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
+                              const unsigned long long* __restrict__ counters_ro, int64_t cap,
+                              const unsigned long long* __restrict__ boff,
+                              const uint32_t* __restrict__ bcnt, const double* __restrict__ gpre,
+                              const int32_t* __restrict__ pk, Cands grp, uint32_t* kept_bm,
+                              Uncertain un, int64_t ucap, uint32_t* req_bm, uint32_t* req_pair,
+                              uint32_t* req_cell, int64_t rcap, unsigned long long* counters) {
+  if ((int64_t)counters_ro[0] > cap) return;
+  const int64_t m = (int64_t)counters_ro[0];
+  const int64_t cells = (int64_t)g.U * g.U;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const int p = (int)grp.pair[i];
+    const uint32_t cell = grp.cell[i];
+    const int k = (int)(cell / g.U), t = (int)(cell % g.U);
+    const int b = (int)grp.bucket[i];
+    const double lat = grp.lat[i], fid = grp.fid[i];
+    const PairConst pc = pcs[p];
+    const int64_t idx = grid_index(g, k, t);
+    bool killed = false, unsure = false;
+
+    // heavy-set twin with more bypass: equal fidelity, strictly lower latency
+    const int kp = pk[k];
+    if (kp >= 0) {
+      const uint32_t* C = slot_cnt(g, pc.slot);
+      const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
+      if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
+        const CellVal tw = eval_cell(g, pc, kp, t);
+        if (tw.lat < lat || (tw.lat == lat && grid_index(g, kp, t) < idx)) killed = true;
+      }
+    }
+    if (!killed) {
+      const double G = gpre[(int64_t)p * g.nbuckets + b];
+      if (G < fid - pc.delta2) killed = true;
+      else if (G <= fid + pc.delta2) unsure = true;
+    }
+    if (!killed) {
+      const int64_t key = (int64_t)p * g.nbuckets + b;
+      const int64_t s0 = (int64_t)boff[key], s1 = s0 + bcnt[key];
+      for (int64_t j = s0; j < s1 && j < m; ++j) {
+        if (j == i) continue;
+        const double ld = grp.lat[j];
+        if (ld > lat) continue;
+        const double fd = grp.fid[j];
+        const uint32_t dc = grp.cell[j];
+        const int kd = (int)(dc / g.U), td = (int)(dc % g.U);
+        if (fabs(fd - fid) > pc.delta2) {
+          if (fd < fid) { killed = true; break; }
+        } else if (same_heavy(g, pc.slot, kd, td, k, t)) {
+          if (ld < lat || grid_index(g, kd, td) < idx) { killed = true; break; }
+        } else {
+          unsure = true;
+        }
+      }
+    }
+    if (killed) continue;
+    if (!unsure) {
+      set_bit(kept_bm, (int64_t)p * g.bm_stride + cell);
+    } else {
+      push_uncertain(0, p, cell, un, ucap, counters);
+      request_exact(cells, p, cell, req_bm, req_pair, req_cell, rcap, counters);
+    }
+  }
+}
+
+// ------------------------------------------------- F7: no-bypass sub-frontier
+
+constexpr int kRowThreads = 1024;
+constexpr int kMaxRowU = 8192;
+
+// theta = max(thresholds) row (rank U-1): cells sorted by tau have
+// non-decreasing latency; equal nr means identical cells (keep smallest index).
+__global__ void __launch_bounds__(kRowThreads)
+nobypass_kernel(Grid g, const PairConst* __restrict__ pcs, uint32_t* kept_bm, Uncertain un,
+                int64_t ucap, uint32_t* req_bm, uint32_t* req_pair, uint32_t* req_cell,
+                int64_t rcap, unsigned long long* counters) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_fid = reinterpret_cast<double*>(smem);            // per group (by start t)
+  double* s_pre = s_fid + g.U;                                 // exclusive prefix-min per t
+  int32_t* s_rep = reinterpret_cast<int32_t*>(s_pre + g.U);    // group representative t
+  int32_t* s_start = s_rep + g.U;                              // group start t for each t
+  const int p = blockIdx.x;
+  const PairConst pc = pcs[p];
+  const uint32_t* C = slot_cnt(g, pc.slot);
+  const int k = g.U - 1;
+  const int64_t rk = (int64_t)k * g.B1;
+  const int64_t cells = (int64_t)g.U * g.U;
+  // group starts: t == 0 or nr changes
+  for (int t = threadIdx.x; t < g.U; t += blockDim.x) {
+    const bool start = (t == 0) || (C[rk + t] != C[rk + t - 1]);
+    s_start[t] = start ? t : -1;
+    s_fid[t] = start ? eval_cell(g, pc, k, t).fid : INFINITY;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // sequential pass over groups (U <= 8192): group ids, representatives, prefix minima
+    int cur = 0;
+    double run = INFINITY;
+    int rep = 0;
+    for (int t = 0; t < g.U; ++t) {
+      if (s_start[t] >= 0) {
+        if (t > 0) { s_rep[cur] = rep; run = fmin(run, s_fid[cur]); }
+        cur = t;
+        rep = t;
+        s_pre[t] = run;
+      } else {
+        s_start[t] = cur;
+        if (g.first_pos[t] < g.first_pos[rep]) rep = t;
+      }
+    }
+    s_rep[cur] = rep;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < g.U; t += blockDim.x) {
+    if (s_start[t] != t) continue;
+    const double f = s_fid[t], m = s_pre[t];
+    const uint32_t cell = (uint32_t)(k * g.U + s_rep[t]);
+    if (m < f - pc.delta2) continue;                   // certainly dominated
+    if (m > f + pc.delta2) {                           // certainly a new minimum
+      set_bit(kept_bm, (int64_t)p * g.bm_stride + cell);
+    } else {
+      push_uncertain(1, p, cell, un, ucap, counters);
+      request_exact(cells, p, cell, req_bm, req_pair, req_cell, rcap, counters);
+    }
+  }
+}
+
+// --------------------------------------- F8: partners of uncertain decisions
+
+__global__ void partners_kernel(Grid g, const PairConst* __restrict__ pcs,
+                                const unsigned long long* __restrict__ counters_ro, int64_t cap,
+                                int64_t ucap, Uncertain un, Cands grp,
+                                const unsigned long long* __restrict__ boff, uint32_t* req_bm,
+                                uint32_t* req_pair, uint32_t* req_cell, int64_t rcap,
+                                unsigned long long* counters) {
+  if ((int64_t)counters_ro[0] > cap) return;
+  const int64_t nu = (int64_t)min((unsigned long long)ucap, counters_ro[1]);
+  const int64_t m = (int64_t)counters_ro[0];
+  const int64_t cells = (int64_t)g.U * g.U;
+  for (int64_t e = blockIdx.x; e < nu; e += gridDim.x) {
+    const int p = (int)un.pair[e];
+    const uint32_t cell = un.cell[e];
+    const int k = (int)(cell / g.U), t = (int)(cell % g.U);
+    const PairConst pc = pcs[p];
+    const CellVal v = eval_cell(g, pc, k, t);
+    if (un.universe[e] == 0) {
+      const int b = bucket_of(pc, g.nbuckets, v.lat);
+      const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
+      const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
+      for (int64_t j = s0 + threadIdx.x; j < s1; j += blockDim.x) {
+        if (grp.lat[j] > v.lat || fabs(grp.fid[j] - v.fid) > pc.delta2) continue;
+        request_exact(cells, p, grp.cell[j], req_bm, req_pair, req_cell, rcap, counters);
+      }
+    } else {
+      const uint32_t* C = slot_cnt(g, pc.slot);
+      const int64_t rk = (int64_t)(g.U - 1) * g.B1;
+      for (int td = threadIdx.x; td < t; td += blockDim.x) {
+        if (td > 0 && C[rk + td] == C[rk + td - 1]) continue;   // group starts only
+        if (C[rk + td] == C[rk + t]) continue;                  // same group as t
+        const CellVal d = eval_cell(g, pc, g.U - 1, td);
+        if (fabs(d.fid - v.fid) > pc.delta2) continue;
+        request_exact(cells, p, (uint32_t)((g.U - 1) * g.U + td), req_bm, req_pair, req_cell,
+                      rcap, counters);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------ F9: numpy-exact fidelities
+
+__global__ void __launch_bounds__(kPwThreads)
+exact_requests_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
+                      const double* __restrict__ h, const double* __restrict__ scores,
+                      const unsigned long long* __restrict__ counters_ro, int64_t rcap,
+                      const uint32_t* __restrict__ req_pair, const uint32_t* __restrict__ req_cell,
+                      double* __restrict__ req_fid) {
+  __shared__ PwShared sh;
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  for (int64_t e = blockIdx.x; e < nr; e += gridDim.x) {
+    const int p = (int)req_pair[e];
+    const uint32_t cell = req_cell[e];
+    const PairConst pc = pcs[p];
+    CellCost c{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
+    const double sum = pw_block_sum(h, scores + (int64_t)pc.slot * g.n, g.n, c, sh);
+    if (threadIdx.x == 0) req_fid[e] = __ddiv_rn(sum, (double)g.n);
+  }
+}
+
+// ------------------------------------------- F10: sort requests by (pair, cell)
+
+constexpr int kSortMax = 2048;
+
+__global__ void __launch_bounds__(1024)
+sort_requests_kernel(const unsigned long long* __restrict__ counters_ro, int64_t rcap,
+                     int64_t cells, uint32_t* req_pair, uint32_t* req_cell, double* req_fid) {
+  __shared__ unsigned long long key[kSortMax];
+  __shared__ double val[kSortMax];
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  if (nr <= 1 || nr > kSortMax) return;
+  int npow = 1;
+  while (npow < nr) npow <<= 1;
+  for (int i = threadIdx.x; i < npow; i += blockDim.x) {
+    key[i] = i < nr ? (unsigned long long)req_pair[i] * cells + req_cell[i] : ~0ull;
+    val[i] = i < nr ? req_fid[i] : 0.0;
+  }
+  __syncthreads();
+  for (int size = 2; size <= npow; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < npow; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          if ((key[i] > key[j]) == up) {
+            unsigned long long tk = key[i]; key[i] = key[j]; key[j] = tk;
+            double tv = val[i]; val[i] = val[j]; val[j] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    req_pair[i] = (uint32_t)(key[i] / cells);
+    req_cell[i] = (uint32_t)(key[i] % cells);
+    req_fid[i] = val[i];
+  }
+}
+
+__device__ bool lookup_exact(int64_t nr, int64_t cells, const uint32_t* req_pair,
+                             const uint32_t* req_cell, const double* req_fid, int p,
+                             uint32_t cell, double* out) {
+  const unsigned long long want = (unsigned long long)p * cells + cell;
+  int64_t lo = 0, hi = nr;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const unsigned long long k = (unsigned long long)req_pair[mid] * cells + req_cell[mid];
+    if (k < want) lo = mid + 1; else hi = mid;
+  }
+  if (lo < nr && (unsigned long long)req_pair[lo] * cells + req_cell[lo] == want) {
+    *out = req_fid[lo];
+    return true;
+  }
+  return false;
+}
+
+// ------------------------------------------- F11: re-decide uncertain cells
+
+__global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
+                               const unsigned long long* __restrict__ counters_ro, int64_t cap,
+                               int64_t ucap, int64_t rcap, Uncertain un, Cands grp,
+                               const unsigned long long* __restrict__ boff,
+                               const uint32_t* __restrict__ req_pair,
+                               const uint32_t* __restrict__ req_cell,
+                               const double* __restrict__ req_fid, uint32_t* kept_bm,
+                               unsigned long long* counters) {
+  __shared__ int s_kill;
+  if ((int64_t)counters_ro[0] > cap) return;
+  const int64_t nu = (int64_t)min((unsigned long long)ucap, counters_ro[1]);
+  const int64_t m = (int64_t)min((unsigned long long)cap, counters_ro[0]);
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  const int64_t cells = (int64_t)g.U * g.U;
+  if (nr > kSortMax) {  // requests were not sorted: report, decide nothing
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&counters[4], 2ull);
+    return;
+  }
+  for (int64_t e = blockIdx.x; e < nu; e += gridDim.x) {
+    const int p = (int)un.pair[e];
+    const uint32_t cell = un.cell[e];
+    const int k = (int)(cell / g.U), t = (int)(cell % g.U);
+    const PairConst pc = pcs[p];
+    const CellVal v = eval_cell(g, pc, k, t);
+    const int64_t idx = grid_index(g, k, t);
+    double fc = 0.0;
+    const bool have_c = lookup_exact(nr, cells, req_pair, req_cell, req_fid, p, cell, &fc);
+    if (threadIdx.x == 0) s_kill = have_c ? 0 : 2;
+    __syncthreads();
+    if (un.universe[e] == 0) {
+      const int b = bucket_of(pc, g.nbuckets, v.lat);
+      const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
+      const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
+      for (int64_t j = s0 + threadIdx.x; j < s1 && have_c; j += blockDim.x) {
+        const uint32_t dc = grp.cell[j];
+        if (dc == cell) continue;
+        const double ld = grp.lat[j];
+        if (ld > v.lat) continue;
+        double fd = grp.fid[j];
+        double fcc = v.fid;
+        if (fabs(fd - v.fid) <= pc.delta2) {
+          if (!lookup_exact(nr, cells, req_pair, req_cell, req_fid, p, dc, &fd)) { atomicMax(&s_kill, 2); continue; }
+          fcc = fc;
+        }
+        if (kills(fd, fcc, ld, v.lat, grid_index(g, (int)(dc / g.U), (int)(dc % g.U)), idx))
+          atomicMax(&s_kill, 1);
+      }
+    } else {
+      const uint32_t* C = slot_cnt(g, pc.slot);
+      const int64_t rk = (int64_t)(g.U - 1) * g.B1;
+      for (int td = threadIdx.x; td < t && have_c; td += blockDim.x) {
+        if (td > 0 && C[rk + td] == C[rk + td - 1]) continue;
+        if (C[rk + td] == C[rk + t]) continue;
+        const CellVal d = eval_cell(g, pc, g.U - 1, td);
+        double fd = d.fid, fcc = v.fid;
+        if (fabs(d.fid - v.fid) <= pc.delta2) {
+          if (!lookup_exact(nr, cells, req_pair, req_cell, req_fid, p,
+                            (uint32_t)((g.U - 1) * g.U + td), &fd)) { atomicMax(&s_kill, 2); continue; }
+          fcc = fc;
+        }
+        if (fd <= fcc) atomicMax(&s_kill, 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_kill == 0) set_bit(kept_bm, (int64_t)p * g.bm_stride + cell);
+      if (s_kill == 2) atomicOr(&counters[4], 4ull);   // missing exact value: overflow
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- F12: emit
+
+__global__ void __launch_bounds__(kScanThreads)
+count_rows_kernel(const uint32_t* __restrict__ kept_bm, int64_t words_per_pair,
+                  unsigned long long* __restrict__ pair_rows) {
+  __shared__ unsigned long long part[kScanThreads];
+  const int p = blockIdx.x;
+  const uint32_t* w = kept_bm + (int64_t)p * words_per_pair;
+  unsigned long long s = 0;
+  for (int64_t i = threadIdx.x; i < words_per_pair; i += blockDim.x) s += __popc(w[i]);
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) part[threadIdx.x] += part[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pair_rows[p] = part[0];
+}
+
+__global__ void pair_offsets_kernel(const unsigned long long* __restrict__ pair_rows, int n_pairs,
+                                    unsigned long long* __restrict__ pair_off, int64_t* stats,
+                                    int64_t out_cap, unsigned long long* counters) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long run = 0;
+  for (int p = 0; p < n_pairs; ++p) {
+    pair_off[p] = run;
+    stats[HADIS_ST_PAIR0 + p] = (int64_t)pair_rows[p];
+    run += pair_rows[p];
+  }
+  pair_off[n_pairs] = run;
+  stats[HADIS_ST_ROWS] = (int64_t)run;
+  stats[HADIS_ST_CANDIDATES] = (int64_t)counters[0];
+  stats[HADIS_ST_UNCERTAIN] = (int64_t)counters[1];
+  stats[HADIS_ST_EXACT_CELLS] = (int64_t)counters[2];
+  if ((int64_t)run > out_cap) counters[4] |= 8ull;
+}
+
+struct Rows {
+  int32_t* pair;
+  int32_t* theta_pos;
+  int32_t* tau_pos;
+  double* r_light;
+  double* r_heavy;
+  double* fid;
+  double* lat;
+  uint32_t* cell;   // workspace: k * U + t, for exact patches
+};
+
+__global__ void __launch_bounds__(kScanThreads)
+emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __restrict__ kept_bm,
+                 int64_t words_per_pair, const unsigned long long* __restrict__ pair_off,
+                 int64_t out_cap, Rows out) {
+  __shared__ unsigned long long part[kScanThreads];
+  const int p = blockIdx.x;
+  const PairConst pc = pcs[p];
+  const uint32_t* w = kept_bm + (int64_t)p * words_per_pair;
+  const int64_t cells = (int64_t)g.U * g.U;
+  unsigned long long base = pair_off[p];
+  const double dn = (double)g.n;
+  for (int64_t w0 = 0; w0 < words_per_pair; w0 += blockDim.x) {
+    const int64_t wi = w0 + threadIdx.x;
+    const uint32_t word = wi < words_per_pair ? w[wi] : 0u;
+    part[threadIdx.x] = __popc(word);
+    __syncthreads();
+    for (int off = 1; off < blockDim.x; off <<= 1) {
+      unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : 0ull;
+      __syncthreads();
+      part[threadIdx.x] += o;
+      __syncthreads();
+    }
+    unsigned long long at = base + part[threadIdx.x] - __popc(word);
+    uint32_t bits = word;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t c = wi * 32 + b;
+      if (c < cells && (int64_t)at < out_cap) {
+        const int k = (int)(c / g.U), t = (int)(c % g.U);
+        const CellVal v = eval_cell(g, pc, k, t);
+        out.pair[at] = p;
+        out.theta_pos[at] = g.first_pos[k];
+        out.tau_pos[at] = g.first_pos[t];
+        out.r_light[at] = __ddiv_rn((double)v.n_keep_light, dn);
+        out.r_heavy[at] = __ddiv_rn((double)v.n_heavy, dn);
+        out.fid[at] = v.fid;
+        out.lat[at] = v.lat;
+        out.cell[at] = (uint32_t)c;
+      }
+      ++at;
+    }
+    const unsigned long long tot = part[blockDim.x - 1];
+    __syncthreads();
+    base += tot;
+  }
+}
+
+// F13: patch rows whose fidelity was computed exactly during resolution
+__global__ void patch_rows_kernel(const unsigned long long* __restrict__ counters_ro, int64_t rcap,
+                                  const uint32_t* __restrict__ req_pair,
+                                  const uint32_t* __restrict__ req_cell,
+                                  const double* __restrict__ req_fid,
+                                  const unsigned long long* __restrict__ pair_off, int64_t out_cap,
+                                  Rows out) {
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  const int p = (int)req_pair[i];
+  const uint32_t cell = req_cell[i];
+  int64_t lo = (int64_t)pair_off[p], hi = (int64_t)pair_off[p + 1];
+  if (hi > out_cap) hi = out_cap;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (out.cell[mid] < cell) lo = mid + 1; else hi = mid;
+  }
+  if (lo < (int64_t)pair_off[p + 1] && lo < out_cap && out.cell[lo] == cell) out.fid[lo] = req_fid[i];
+}
+
+// F14: exact_fid mode -- numpy-exact fidelity for every emitted row
+__global__ void __launch_bounds__(kPwThreads)
+exact_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
+                  const double* __restrict__ h, const double* __restrict__ scores,
+                  const unsigned long long* __restrict__ pair_off, int n_pairs, int64_t out_cap,
+                  Rows out) {
+  __shared__ PwShared sh;
+  int64_t rows = (int64_t)pair_off[n_pairs];
+  if (rows > out_cap) rows = out_cap;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int p = out.pair[r];
+    const uint32_t cell = out.cell[r];
+    const PairConst pc = pcs[p];
+    CellCost c{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
+    const double sum = pw_block_sum(h, scores + (int64_t)pc.slot * g.n, g.n, c, sh);
+    if (threadIdx.x == 0) out.fid[r] = __ddiv_rn(sum, (double)g.n);
+  }
+}
+
+__global__ void finish_stats_kernel(const unsigned long long* counters, int64_t cap, int64_t ucap,
+                                    int64_t rcap, int64_t* stats) {
+  unsigned long long of = counters[4];
+  if ((int64_t)counters[0] > cap) of |= 16ull;
+  if ((int64_t)counters[1] > ucap) of |= 32ull;
+  if ((int64_t)counters[2] > rcap) of |= 64ull;
+  stats[HADIS_ST_OVERFLOW] = (int64_t)of;
+}
+
+// ------------------------------------------------ explicit-cell exact means
+
+__global__ void __launch_bounds__(kPwThreads)
+fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
+                 int n_cells, const int32_t* __restrict__ slot, const double* __restrict__ theta,
+                 const double* __restrict__ tau, const double* __restrict__ params,
+                 double* __restrict__ out) {
+  __shared__ PwShared sh;
+  for (int c = blockIdx.x; c < n_cells; c += gridDim.x) {
+    const double* q = params + (int64_t)c * 4;
+    CellCost cc{theta[c], tau[c], q[0], q[1], q[2], q[3]};
+    const double sum = pw_block_sum(h, scores + (int64_t)slot[c] * n, n, cc, sh);
+    if (threadIdx.x == 0) out[c] = __ddiv_rn(sum, (double)n);
+  }
+}
+
+// ------------------------------------------------------------ workspace
+
+struct Layout {
+  size_t pcs, pk, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
+      counters, pair_rows, pair_off, row_cell, total;
+};
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t ecap,
+                          int64_t out_cap) {
+  Layout L{};
+  size_t at = 0;
+  auto take = [&](size_t bytes) { size_t r = at; at = align_up(at + bytes); return r; };
+  const int64_t pb = (int64_t)n_pairs * nbuckets;
+  const int64_t cells = (int64_t)U * U;
+  const int64_t words = (cells + 31) / 32 * n_pairs;
+  L.pcs = take(sizeof(PairConst) * n_pairs);
+  L.pk = take(sizeof(int32_t) * U);
+  L.bmin = take(8 * pb);
+  L.gpre = take(8 * pb);
+  L.bcnt = take(4 * pb);
+  L.bcur = take(4 * pb);
+  L.boff = take(8 * (pb + 1));
+  L.raw[0] = take(4 * cap); L.raw[1] = take(4 * cap); L.raw[2] = take(4 * cap);
+  L.raw[3] = take(8 * cap); L.raw[4] = take(8 * cap);
+  L.grp[0] = take(4 * cap); L.grp[1] = take(4 * cap); L.grp[2] = take(4 * cap);
+  L.grp[3] = take(8 * cap); L.grp[4] = take(8 * cap);
+  L.kept = take(4 * words);
+  L.reqbm = take(4 * words);
+  L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
+  L.req[0] = take(4 * ecap); L.req[1] = take(4 * ecap); L.req[2] = take(8 * ecap);
+  L.counters = take(8 * 8);
+  L.pair_rows = take(8 * n_pairs);
+  L.pair_off = take(8 * (n_pairs + 1));
+  L.row_cell = take(4 * out_cap);
+  L.total = at;
+  return L;
+}
+
+static int buckets_for(int U) {
+  int64_t cells = (int64_t)U * U;
+  int64_t b = 1024;
+  while (b < cells / 8 && b < (1 << 17)) b <<= 1;
+  return (int)b;
+}
+
+}  // namespace hadis
+
+using namespace hadis;
+
+extern "C" size_t hadis_frontier_workspace_bytes(int32_t n_pairs, int32_t n_unique,
+                                                 int64_t cand_cap, int64_t exact_cap,
+                                                 int64_t out_cap) {
+  if (n_pairs <= 0 || n_unique <= 0 || cand_cap <= 0 || exact_cap <= 0 || out_cap <= 0) return 0;
+  return make_layout(n_pairs, n_unique, buckets_for(n_unique), cand_cap, exact_cap, out_cap).total;
+}
+
+extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
+                                    int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
+                                    const int32_t* pair_slot, const double* pair_params,
+                                    const int32_t* first_pos, int32_t n_thresholds,
+                                    const double* thr_unique, const double* h,
+                                    const double* scores, int32_t exact_fid, void* workspace,
+                                    size_t workspace_bytes, int64_t cand_cap, int64_t exact_cap,
+                                    int64_t out_cap, int32_t* out_pair, int32_t* out_theta_pos,
+                                    int32_t* out_tau_pos, double* out_r_light,
+                                    double* out_r_heavy, double* out_fid, double* out_lat,
+                                    int64_t* stats, void* stream) {
+  if (!pre_cnt || !pre_hsum || n <= 0 || n > 0xffffffffll || n_unique <= 0 ||
+      n_unique > kMaxRowU || n_pairs <= 0 || !pair_slot || !pair_params || !first_pos ||
+      n_thresholds < n_unique || !thr_unique || !h || !scores || !workspace || cand_cap <= 0 ||
+      exact_cap <= 0 || out_cap <= 0 || !stats)
+    return HADIS_ERR_ARG;
+  if ((int64_t)n_unique * n_unique > 0xffffffffll) return HADIS_ERR_UNSUPPORTED;
+  const int nb = buckets_for(n_unique);
+  const Layout L = make_layout(n_pairs, n_unique, nb, cand_cap, exact_cap, out_cap);
+  if (workspace_bytes < L.total) return HADIS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  auto P = [&](size_t off) { return (void*)(ws + off); };
+
+  PairConst* pcs = (PairConst*)P(L.pcs);
+  int32_t* pk = (int32_t*)P(L.pk);
+  unsigned long long* bmin = (unsigned long long*)P(L.bmin);
+  double* gpre = (double*)P(L.gpre);
+  uint32_t* bcnt = (uint32_t*)P(L.bcnt);
+  uint32_t* bcur = (uint32_t*)P(L.bcur);
+  unsigned long long* boff = (unsigned long long*)P(L.boff);
+  Cands raw{(uint32_t*)P(L.raw[0]), (uint32_t*)P(L.raw[1]), (uint32_t*)P(L.raw[2]),
+            (double*)P(L.raw[3]), (double*)P(L.raw[4])};
+  Cands grp{(uint32_t*)P(L.grp[0]), (uint32_t*)P(L.grp[1]), (uint32_t*)P(L.grp[2]),
+            (double*)P(L.grp[3]), (double*)P(L.grp[4])};
+  uint32_t* kept = (uint32_t*)P(L.kept);
+  uint32_t* reqbm = (uint32_t*)P(L.reqbm);
+  Uncertain un{(uint32_t*)P(L.un[0]), (uint32_t*)P(L.un[1]), (uint32_t*)P(L.un[2])};
+  uint32_t* req_pair = (uint32_t*)P(L.req[0]);
+  uint32_t* req_cell = (uint32_t*)P(L.req[1]);
+  double* req_fid = (double*)P(L.req[2]);
+  unsigned long long* counters = (unsigned long long*)P(L.counters);
+  unsigned long long* pair_rows = (unsigned long long*)P(L.pair_rows);
+  unsigned long long* pair_off = (unsigned long long*)P(L.pair_off);
+  uint32_t* row_cell = (uint32_t*)P(L.row_cell);
+
+  const int64_t pb = (int64_t)n_pairs * nb;
+  const int64_t cells = (int64_t)n_unique * n_unique;
+  const int64_t words_per_pair = (cells + 31) / 32;
+  HADIS_CUDA_TRY(cudaMemsetAsync(bmin, 0xff, 8 * pb, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(bcnt, 0, 4 * pb, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(bcur, 0, 4 * pb, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(kept, 0, 4 * words_per_pair * n_pairs, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(reqbm, 0, 4 * words_per_pair * n_pairs, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * 8, st));
+
+  Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
+         n_thresholds, first_pos, words_per_pair * 32};
+  pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
+      n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
+  twin_row_kernel<<<1, 1, 0, st>>>(pre_cnt + (int64_t)0, n_unique, n_unique + 1, pk);
+  HADIS_LAUNCH_CHECK();
+
+  const int64_t total_cells = cells * n_pairs;
+  int64_t grid_cells = ceil_div(total_cells, kCellThreads);
+  if (grid_cells > (int64_t)kNumSMs * 16) grid_cells = (int64_t)kNumSMs * 16;
+  bucket_min_kernel<<<(unsigned)grid_cells, kCellThreads, 0, st>>>(g, pcs, n_pairs, bmin);
+  bucket_prefix_kernel<<<n_pairs, kScanThreads, 0, st>>>(bmin, nb, gpre);
+  filter_kernel<<<(unsigned)grid_cells, kCellThreads, 0, st>>>(g, pcs, n_pairs, gpre, bcnt, raw,
+                                                              cand_cap, counters);
+  exclusive_scan_kernel<<<1, kScanThreads, 0, st>>>(bcnt, pb, boff);
+  scatter_kernel<<<kNumSMs * 4, 256, 0, st>>>(raw, counters, cand_cap, nb, boff, bcur, grp);
+  HADIS_LAUNCH_CHECK();
+  decide_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre, pk,
+                                             grp, kept, un, exact_cap, reqbm, req_pair, req_cell,
+                                             exact_cap, counters);
+  const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
+  if (row_smem > 48 * 1024)
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(nobypass_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem));
+  nobypass_kernel<<<n_pairs, kRowThreads, row_smem, st>>>(g, pcs, kept, un, exact_cap, reqbm,
+                                                          req_pair, req_cell, exact_cap, counters);
+  HADIS_LAUNCH_CHECK();
+  partners_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, un, grp, boff,
+                                           reqbm, req_pair, req_cell, exact_cap, counters);
+  exact_requests_kernel<<<kNumSMs * 2, kPwThreads, 0, st>>>(g, pcs, thr_unique, h, scores,
+                                                            counters, exact_cap, req_pair,
+                                                            req_cell, req_fid);
+  sort_requests_kernel<<<1, 1024, 0, st>>>(counters, exact_cap, cells, req_pair, req_cell,
+                                           req_fid);
+  resolve_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, exact_cap, un,
+                                          grp, boff, req_pair, req_cell, req_fid, kept, counters);
+  HADIS_LAUNCH_CHECK();
+  count_rows_kernel<<<n_pairs, kScanThreads, 0, st>>>(kept, words_per_pair, pair_rows);
+  pair_offsets_kernel<<<1, 1, 0, st>>>(pair_rows, n_pairs, pair_off, stats, out_cap, counters);
+  Rows out{out_pair, out_theta_pos, out_tau_pos, out_r_light, out_r_heavy, out_fid, out_lat,
+           row_cell};
+  emit_rows_kernel<<<n_pairs, kScanThreads, 0, st>>>(g, pcs, kept, words_per_pair, pair_off,
+                                                     out_cap, out);
+  if (exact_fid) {
+    exact_rows_kernel<<<kNumSMs * 2, kPwThreads, 0, st>>>(g, pcs, thr_unique, h, scores,
+                                                          pair_off, n_pairs, out_cap, out);
+  } else {
+    patch_rows_kernel<<<(unsigned)ceil_div(exact_cap, 256), 256, 0, st>>>(
+        counters, exact_cap, req_pair, req_cell, req_fid, pair_off, out_cap, out);
+  }
+  finish_stats_kernel<<<1, 1, 0, st>>>(counters, cand_cap, exact_cap, exact_cap, stats);
+  HADIS_LAUNCH_CHECK();
+  return HADIS_OK;
+}
+
+extern "C" int hadis_fid_exact(const double* h, const double* scores, int64_t n, int32_t n_cells,
+                               const int32_t* cell_slot, const double* cell_theta,
+                               const double* cell_tau, const double* cell_params, double* out_fid,
+                               void* stream) {
+  if (!h || !scores || n <= 0 || n_cells < 0 || (n_cells > 0 && (!cell_slot || !cell_theta ||
+      !cell_tau || !cell_params || !out_fid)))
+    return HADIS_ERR_ARG;
+  if (n_cells == 0) return HADIS_OK;
+  int grid = n_cells < kNumSMs * 4 ? n_cells : kNumSMs * 4;
+  fid_exact_kernel<<<grid, kPwThreads, 0, (cudaStream_t)stream>>>(
+      h, scores, n, n_cells, cell_slot, cell_theta, cell_tau, cell_params, out_fid);
+  HADIS_LAUNCH_CHECK();
+  return HADIS_OK;
+}

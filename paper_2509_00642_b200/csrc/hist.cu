@@ -1,0 +1,207 @@
+// K1 (bin + 2-D histogram) and K2 (2-D prefix scan) of the cascade profiler.
+//
+// Reference semantics (pkg/src/cascadesim/profiler.py):
+//   bypass(q, theta) = h[q] > theta                       (:138)
+//   reject(q, tau)   = not bypass and score_light[q] < tau (:149)
+// With u = the sorted distinct threshold values (size U) we bin
+//   bh(q) = #{u < h[q]}          -> bypass at theta = u[k]  <=>  bh > k
+//   bs(q) = #{u <= s[q]}         -> s < tau = u[t]          <=>  bs <= t
+// so every grid cell (k, t) is a union of histogram bins and all counts and
+// hardness sums follow from 2-D prefix sums of an (U+1) x (U+1) histogram per
+// light model.  Integer accumulation (counts u32, hardness in fixed point
+// 2^-shift as u64) is exact and order independent, hence deterministic.
+#include "common.cuh"
+
+namespace hadis {
+
+constexpr int kHistThreads = 512;
+constexpr int kMaxSmemThr = 8192;  // thresholds staged in shared memory up to this
+
+// Shared-memory privatised variant: all light models' histograms fit on chip.
+__global__ void __launch_bounds__(kHistThreads)
+bin_hist_smem_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
+                     int n_light, const double* __restrict__ thr, int U, double hscale,
+                     uint32_t* __restrict__ g_cnt, unsigned long long* __restrict__ g_hsum,
+                     uint32_t* __restrict__ bad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int B1 = U + 1;
+  const int bins = B1 * B1 * n_light;
+  unsigned long long* s_hsum = reinterpret_cast<unsigned long long*>(smem);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_hsum + bins);
+  double* s_thr = reinterpret_cast<double*>(s_cnt + ((bins + 1) & ~1));
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) { s_hsum[i] = 0; s_cnt[i] = 0; }
+  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+  __syncthreads();
+
+  uint32_t my_bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const double hq = h[q];
+    const bool ok = hq >= 0.0 && hq <= 1.0;
+    my_bad += !ok;
+    const int bh = count_less(s_thr, U, hq);
+    const unsigned long long hf = (unsigned long long)__dmul_rn(ok ? hq : 0.0, hscale);
+    for (int l = 0; l < n_light; ++l) {
+      const int bs = count_less_equal(s_thr, U, scores[(int64_t)l * n + q]);
+      const int bin = (l * B1 + bh) * B1 + bs;
+      atomicAdd(&s_cnt[bin], 1u);
+      atomicAdd(&s_hsum[bin], hf);
+    }
+  }
+  if (my_bad) atomicAdd(bad, my_bad);
+  __syncthreads();
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) {
+    if (s_cnt[i]) {
+      atomicAdd(&g_cnt[i], s_cnt[i]);
+      atomicAdd(&g_hsum[i], s_hsum[i]);
+    }
+  }
+}
+
+// Global-memory variant for large grids: L2-resident histograms, integer REDs.
+__global__ void __launch_bounds__(kHistThreads)
+bin_hist_global_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
+                       int n_light, const double* __restrict__ thr, int U, double hscale,
+                       uint32_t* __restrict__ g_cnt, unsigned long long* __restrict__ g_hsum,
+                       uint32_t* __restrict__ bad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_thr = reinterpret_cast<double*>(smem);
+  const bool staged = U <= kMaxSmemThr;
+  if (staged) {
+    for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+    __syncthreads();
+  }
+  const double* u = staged ? s_thr : thr;
+  const int64_t B1 = U + 1;
+  uint32_t my_bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const double hq = h[q];
+    const bool ok = hq >= 0.0 && hq <= 1.0;
+    my_bad += !ok;
+    const int bh = count_less(u, U, hq);
+    const unsigned long long hf = (unsigned long long)__dmul_rn(ok ? hq : 0.0, hscale);
+    for (int l = 0; l < n_light; ++l) {
+      const int bs = count_less_equal(u, U, scores[(int64_t)l * n + q]);
+      const int64_t bin = ((int64_t)l * B1 + bh) * B1 + bs;
+      atomicAdd(&g_cnt[bin], 1u);
+      atomicAdd(&g_hsum[bin], hf);
+    }
+  }
+  if (my_bad) atomicAdd(bad, my_bad);
+}
+
+// K2a: inclusive prefix along bs (the contiguous axis): one warp per row.
+__global__ void scan_rows_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs,
+                                 int64_t rows, int B1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= rows) return;
+  uint32_t* c = cnt + row * B1;
+  unsigned long long* s = hs + row * B1;
+  uint32_t carry_c = 0;
+  unsigned long long carry_s = 0;
+  for (int base = 0; base < B1; base += 32) {
+    const int i = base + lane;
+    uint32_t vc = i < B1 ? c[i] : 0u;
+    unsigned long long vs = i < B1 ? s[i] : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint32_t oc = __shfl_up_sync(0xffffffffu, vc, off);
+      unsigned long long os = __shfl_up_sync(0xffffffffu, vs, off);
+      if (lane >= off) { vc += oc; vs += os; }
+    }
+    vc += carry_c;
+    vs += carry_s;
+    if (i < B1) { c[i] = vc; s[i] = vs; }
+    carry_c = __shfl_sync(0xffffffffu, vc, 31);
+    carry_s = __shfl_sync(0xffffffffu, vs, 31);
+  }
+}
+
+// K2b: inclusive prefix along bh: one thread per (light slot, column),
+// coalesced across columns, rows walked in order.
+__global__ void scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs,
+                                 int n_light, int B1) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= (int64_t)n_light * B1) return;
+  const int64_t l = col / B1, t = col % B1;
+  uint32_t* c = cnt + l * B1 * B1 + t;
+  unsigned long long* s = hs + l * B1 * B1 + t;
+  uint32_t acc_c = 0;
+  unsigned long long acc_s = 0;
+  for (int k = 0; k < B1; ++k) {
+    acc_c += c[(int64_t)k * B1];
+    acc_s += s[(int64_t)k * B1];
+    c[(int64_t)k * B1] = acc_c;
+    s[(int64_t)k * B1] = acc_s;
+  }
+}
+
+}  // namespace hadis
+
+using namespace hadis;
+
+extern "C" int hadis_hfix_shift(int64_t n) {
+  if (n <= 0) return 62;
+  int bits = 0;
+  while ((n >> bits) != 0) ++bits;
+  int shift = 63 - bits;
+  return shift > 62 ? 62 : shift;
+}
+
+extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_light,
+                              const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
+                              uint32_t* hist_cnt, uint64_t* hist_hsum, uint32_t* bad_records,
+                              void* stream) {
+  if (n <= 0 || n > 0xffffffffll || n_light <= 0 || n_unique <= 0 || !h || !scores ||
+      !thr_unique || !hist_cnt || !hist_hsum || !bad_records || hfix_shift < 1 || hfix_shift > 62)
+    return HADIS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t B1 = (int64_t)n_unique + 1;
+  const int64_t bins = B1 * B1 * n_light;
+  HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(bad_records, 0, sizeof(uint32_t), st));
+  const double hscale = ldexp(1.0, hfix_shift);
+  const size_t smem_priv = (size_t)bins * 12 + 8 + (size_t)n_unique * 8;
+  const int64_t blocks_needed = ceil_div(n, kHistThreads);
+  if (smem_priv <= 160 * 1024) {
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_smem_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int per_sm = smem_priv <= 48 * 1024 ? 4 : (smem_priv <= 100 * 1024 ? 2 : 1);
+    int64_t grid = (int64_t)kNumSMs * per_sm;
+    if (grid > blocks_needed) grid = blocks_needed;
+    bin_hist_smem_kernel<<<(unsigned)grid, kHistThreads, smem_priv, st>>>(
+        h, scores, n, n_light, thr_unique, n_unique, hscale, hist_cnt,
+        (unsigned long long*)hist_hsum, bad_records);
+  } else {
+    const size_t smem = n_unique <= kMaxSmemThr ? (size_t)n_unique * 8 : 0;
+    if (smem > 48 * 1024)
+      HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_global_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int64_t grid = (int64_t)kNumSMs * 4;
+    if (grid > blocks_needed) grid = blocks_needed;
+    bin_hist_global_kernel<<<(unsigned)grid, kHistThreads, smem, st>>>(
+        h, scores, n, n_light, thr_unique, n_unique, hscale, hist_cnt,
+        (unsigned long long*)hist_hsum, bad_records);
+  }
+  HADIS_LAUNCH_CHECK();
+  return HADIS_OK;
+}
+
+extern "C" int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t n_light,
+                               int32_t n_unique, void* stream) {
+  if (!hist_cnt || !hist_hsum || n_light <= 0 || n_unique <= 0) return HADIS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B1 = n_unique + 1;
+  const int64_t rows = (int64_t)n_light * B1;
+  scan_rows_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(
+      hist_cnt, (unsigned long long*)hist_hsum, rows, B1);
+  HADIS_LAUNCH_CHECK();
+  const int64_t cols = (int64_t)n_light * B1;
+  scan_cols_kernel<<<(unsigned)ceil_div(cols, 128), 128, 0, st>>>(
+      hist_cnt, (unsigned long long*)hist_hsum, n_light, B1);
+  HADIS_LAUNCH_CHECK();
+  return HADIS_OK;
+}

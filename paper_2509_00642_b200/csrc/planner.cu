@@ -1,0 +1,312 @@
+// K5: allocation search -- planner.solve over many (demand, SLO) points.
+//
+// Reference: pkg/src/cascadesim/planner.py
+//   queue_delay       :81-85   alpha * Q / max(rate, 0.01), 0 when Q <= 0
+//   _path_terms       :93-104  sum(latency + drain) over the row's models
+//   _min_workers      :107-110 max(1, ceil((rate - 1e-9) / mu)), 1 when rate <= 0
+//   _evaluate_row     :113-148 per row min (total, path), first combo wins
+//   _solve_over_rows  :151-167 min (fidelity, total, path, row index)
+//   fallback_plan     :170-214 max bottleneck capacity over worker splits,
+//                              key (-capacity, L_light[1], L_heavy[1], row index)
+//   solve             :217-227 negative demand -> PlannerError
+// One thread evaluates one (point, row) -- all batch combos -- and CTAs reduce
+// to a per-(point, CTA) best; a second kernel reduces the CTA partials.  All
+// float64 operations are the reference's, in its order, without FMA.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace hadis {
+
+constexpr int kPlanThreads = 256;
+constexpr int kMaxBatch = 16;
+constexpr double kSlack = 1e-9;
+constexpr double kRateFloor = 0.01;
+
+struct Best {
+  double k0;      // fidelity (solve) or -capacity (fallback)
+  double k1;      // total workers (solve) or latency_s[1] light (fallback)
+  double k2;      // path latency (solve) or latency_s[1] heavy (fallback)
+  int32_t row;    // -1 = none
+  int32_t xl, xh, bl, bh;
+  double path;
+};
+
+__device__ __forceinline__ bool better(const Best& a, const Best& b) {
+  if (a.row < 0) return false;
+  if (b.row < 0) return true;
+  if (a.k0 != b.k0) return a.k0 < b.k0;
+  if (a.k1 != b.k1) return a.k1 < b.k1;
+  if (a.k2 != b.k2) return a.k2 < b.k2;
+  return a.row < b.row;
+}
+
+struct PlanIn {
+  int n_rows;
+  const int32_t* row_model;
+  const double* row_share;
+  const double* row_fid;
+  int n_models, n_batch;
+  const int32_t* batch;
+  const double* lat;
+  const double* mu;
+  const double* lat1;
+  int n_points;
+  const double* lam;
+  const double* t_slo;
+  const int32_t* workers;
+  const double* queues;
+  double alpha;
+};
+
+__device__ __forceinline__ double drain(double q, double rate, double alpha) {
+  if (!(q > 0.0)) return 0.0;
+  const double r = rate > kRateFloor ? rate : (rate == kRateFloor ? rate : kRateFloor);
+  return __ddiv_rn(__dmul_rn(alpha, q), r);
+}
+
+__device__ __forceinline__ int64_t min_workers(double rate, double mu) {
+  if (rate <= 0.0) return 1;
+  const double need = ceil(__ddiv_rn(__dadd_rn(rate, -kSlack), mu));
+  if (!(need < 4.0e18)) return (int64_t)4e18;
+  const int64_t x = (int64_t)need;
+  return x > 1 ? x : 1;
+}
+
+struct RowShape {
+  int ml, mh;          // model indices
+  bool single;         // light == heavy
+  double sl, sh;       // shares (sh unused when single)
+  bool al, ah;         // active flags
+};
+
+__device__ __forceinline__ RowShape row_shape(const PlanIn& in, int r) {
+  RowShape s;
+  s.ml = in.row_model[2 * r];
+  s.mh = in.row_model[2 * r + 1];
+  s.single = s.ml == s.mh;
+  const double rl = in.row_share[2 * r], rh = in.row_share[2 * r + 1];
+  if (s.single) {
+    s.sl = __dadd_rn(rl, rh);
+    s.sh = 0.0;
+  } else {
+    s.sl = rl;
+    s.sh = __dadd_rn(0.0, rh);
+  }
+  s.al = s.sl > 0.0;
+  s.ah = !s.single && s.sh > 0.0;
+  return s;
+}
+
+// path latency of the row's models at batch indices (il, ih) -- planner.py:93-104
+__device__ __forceinline__ double path_latency(const PlanIn& in, const RowShape& s, int p, int il,
+                                               int ih, double lamv) {
+  const double* Q = in.queues + (int64_t)p * in.n_models;
+  double path = __dadd_rn(0.0, __dadd_rn(in.lat[s.ml * in.n_batch + il],
+                                         drain(Q[s.ml], __dmul_rn(lamv, s.sl), in.alpha)));
+  if (!s.single)
+    path = __dadd_rn(path, __dadd_rn(in.lat[s.mh * in.n_batch + ih],
+                                     drain(Q[s.mh], __dmul_rn(lamv, s.sh), in.alpha)));
+  return path;
+}
+
+__device__ Best eval_row(const PlanIn& in, int p, int r) {
+  Best best;
+  best.row = -1;
+  const RowShape s = row_shape(in, r);
+  const double lamv = in.lam[p];
+  const int W = in.workers[p];
+  const double limit = __dadd_rn(in.t_slo[p], kSlack);
+  const int nl = s.al ? in.n_batch : 1;
+  const int nh = s.ah ? in.n_batch : 1;
+  double best_total = 0.0, best_path = 0.0;
+  for (int il = 0; il < nl; ++il) {
+    int64_t xl = 0;
+    if (s.al) xl = min_workers(__dmul_rn(lamv, s.sl), in.mu[s.ml * in.n_batch + il]);
+    for (int ih = 0; ih < nh; ++ih) {
+      int64_t xh = 0;
+      if (s.ah) xh = min_workers(__dmul_rn(lamv, s.sh), in.mu[s.mh * in.n_batch + ih]);
+      const int64_t total = xl + xh;
+      if (total > W) continue;
+      const double path = path_latency(in, s, p, il, ih, lamv);
+      if (path > limit) continue;
+      const double tot = (double)total;
+      if (best.row < 0 || tot < best_total || (tot == best_total && path < best_path)) {
+        best.row = r;
+        best_total = tot;
+        best_path = path;
+        best.xl = (int32_t)xl;
+        best.xh = (int32_t)xh;
+        best.bl = il;
+        best.bh = ih;
+      }
+    }
+  }
+  if (best.row >= 0) {
+    best.k0 = in.row_fid[r];
+    best.k1 = best_total;
+    best.k2 = best_path;
+    best.path = best_path;
+  }
+  return best;
+}
+
+// fallback_plan candidate of one row (planner.py:179-208)
+__device__ Best fallback_row(const PlanIn& in, int p, int r) {
+  Best best;
+  best.row = -1;
+  const RowShape s = row_shape(in, r);
+  if (!s.al && !s.ah) return best;
+  const int W = in.workers[p];
+  const double lamv = in.lam[p];
+  const double lat_l = in.lat1[s.ml], lat_h = in.lat1[s.mh];
+  const int nl = s.al ? in.n_batch : 1;
+  const int nh = s.ah ? in.n_batch : 1;
+  const bool two = s.al && s.ah;
+  for (int il = 0; il < nl; ++il) {
+    for (int ih = 0; ih < nh; ++ih) {
+      const double mul = s.al ? in.mu[s.ml * in.n_batch + il] : 0.0;
+      const double muh = s.ah ? in.mu[s.mh * in.n_batch + ih] : 0.0;
+      const int i0 = two ? 1 : 0, i1 = two ? W - 1 : 0;
+      for (int i = i0; i <= i1; ++i) {
+        int xl, xh;
+        double cap;
+        if (two) {
+          xl = i;
+          xh = W - i;
+          const double cl = __ddiv_rn(__dmul_rn((double)xl, mul), s.sl);
+          const double ch = __ddiv_rn(__dmul_rn((double)xh, muh), s.sh);
+          cap = ch < cl ? ch : cl;
+        } else if (s.al) {
+          xl = W; xh = 0;
+          cap = __ddiv_rn(__dmul_rn((double)W, mul), s.sl);
+        } else {
+          xl = 0; xh = W;
+          cap = __ddiv_rn(__dmul_rn((double)W, muh), s.sh);
+        }
+        Best c;
+        c.k0 = -cap; c.k1 = lat_l; c.k2 = lat_h; c.row = r;
+        c.xl = xl; c.xh = xh; c.bl = il; c.bh = ih;
+        if (better(c, best)) {
+          c.path = path_latency(in, s, p, il, ih, lamv);
+          best = c;
+        }
+      }
+    }
+  }
+  return best;
+}
+
+__device__ void block_reduce_store(Best mine, Best* out) {
+  __shared__ Best sh[kPlanThreads];
+  sh[threadIdx.x] = mine;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off && better(sh[threadIdx.x + off], sh[threadIdx.x]))
+      sh[threadIdx.x] = sh[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// grid: (row blocks, points)
+__global__ void __launch_bounds__(kPlanThreads)
+solve_rows_kernel(PlanIn in, int fallback, const int32_t* __restrict__ need_fb,
+                  Best* __restrict__ partial) {
+  const int p = blockIdx.y;
+  if (fallback && !need_fb[p]) return;
+  Best mine;
+  mine.row = -1;
+  if (in.lam[p] >= 0.0) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < in.n_rows;
+         r += gridDim.x * blockDim.x) {
+      const Best c = fallback ? fallback_row(in, p, r) : eval_row(in, p, r);
+      if (better(c, mine)) mine = c;
+    }
+  }
+  block_reduce_store(mine, partial + (int64_t)p * gridDim.x + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+reduce_points_kernel(PlanIn in, int fallback, int nblk, const Best* __restrict__ partial,
+                     int32_t* __restrict__ need_fb, int32_t* plan_row, int32_t* plan_x,
+                     int32_t* plan_b, double* plan_path, int32_t* plan_flags) {
+  const int p = blockIdx.x;
+  if (fallback && !need_fb[p]) return;
+  Best mine;
+  mine.row = -1;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    const Best c = partial[(int64_t)p * nblk + b];
+    if (better(c, mine)) mine = c;
+  }
+  __shared__ Best res;
+  block_reduce_store(mine, &res);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (in.lam[p] < 0.0) {
+    plan_row[p] = -1;
+    plan_flags[p] = 2;
+    need_fb[p] = 0;
+    return;
+  }
+  if (!fallback) {
+    need_fb[p] = res.row < 0;
+    if (res.row < 0) return;
+  }
+  plan_row[p] = res.row;
+  if (res.row >= 0) {
+    plan_x[2 * p] = res.xl;
+    plan_x[2 * p + 1] = res.xh;
+    plan_b[2 * p] = in.batch[res.bl];
+    plan_b[2 * p + 1] = in.batch[res.bh];
+    plan_path[p] = res.path;
+  }
+  plan_flags[p] = fallback ? 1 : 0;
+}
+
+}  // namespace hadis
+
+using namespace hadis;
+
+static int plan_blocks(int n_rows) {
+  int b = (n_rows + kPlanThreads - 1) / kPlanThreads;
+  if (b < 1) b = 1;
+  if (b > 64) b = 64;
+  return b;
+}
+
+extern "C" size_t hadis_solve_workspace_bytes(int32_t n_points, int32_t n_rows) {
+  if (n_points <= 0 || n_rows <= 0) return 0;
+  return (size_t)n_points * plan_blocks(n_rows) * sizeof(Best) + (size_t)n_points * 4 + 256;
+}
+
+extern "C" int hadis_solve_many(int32_t n_rows, const int32_t* row_model, const double* row_share,
+                                const double* row_fid, int32_t n_models, int32_t n_batch,
+                                const int32_t* batch_sizes, const double* lat, const double* mu,
+                                const double* lat1, int32_t n_points, const double* lam,
+                                const double* t_slo, const int32_t* workers, const double* queues,
+                                double alpha, int32_t* plan_row, int32_t* plan_x, int32_t* plan_b,
+                                double* plan_path, int32_t* plan_flags, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (n_rows <= 0 || n_points <= 0 || n_models <= 0 || n_batch <= 0 || n_batch > kMaxBatch ||
+      !row_model || !row_share || !row_fid || !batch_sizes || !lat || !mu || !lat1 || !lam ||
+      !t_slo || !workers || !queues || !plan_row || !plan_x || !plan_b || !plan_path ||
+      !plan_flags || !workspace || n_points > 65535)
+    return HADIS_ERR_ARG;
+  if (workspace_bytes < hadis_solve_workspace_bytes(n_points, n_rows)) return HADIS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblk = plan_blocks(n_rows);
+  Best* partial = (Best*)workspace;
+  int32_t* need_fb = (int32_t*)((char*)workspace + (size_t)n_points * nblk * sizeof(Best));
+  PlanIn in{n_rows, row_model, row_share, row_fid, n_models, n_batch, batch_sizes, lat, mu,
+            lat1, n_points, lam, t_slo, workers, queues, alpha};
+  dim3 grid(nblk, n_points);
+  solve_rows_kernel<<<grid, kPlanThreads, 0, st>>>(in, 0, need_fb, partial);
+  reduce_points_kernel<<<n_points, kPlanThreads, 0, st>>>(in, 0, nblk, partial, need_fb, plan_row,
+                                                          plan_x, plan_b, plan_path, plan_flags);
+  solve_rows_kernel<<<grid, kPlanThreads, 0, st>>>(in, 1, need_fb, partial);
+  reduce_points_kernel<<<n_points, kPlanThreads, 0, st>>>(in, 1, nblk, partial, need_fb, plan_row,
+                                                          plan_x, plan_b, plan_path, plan_flags);
+  HADIS_LAUNCH_CHECK();
+  return HADIS_OK;
+}

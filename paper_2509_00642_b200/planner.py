@@ -1,0 +1,264 @@
+"""Online allocation search on the GPU: drop-in for cascadesim.planner.solve.
+
+Public surface mirrors pkg/src/cascadesim/planner.py:
+``Plan`` (:40-78), ``PlannerError`` (:36), ``queue_delay`` (:81),
+``update_estimate`` (:88), ``solve`` (:217-227), ``fallback_plan``
+(:170-214) and ``make_planner(mode="online")`` (:443-455), plus the batched
+``solve_many`` used by re-plan sweeps.  Every (demand, SLO) point is decided
+on the device by ``hadis_solve_many`` with the reference's exact float64
+expressions and tie-breaks; this module only moves rows/points to the device
+and turns the per-point result back into ``Plan`` objects.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+DEFAULT_WORKERS = 16
+DEFAULT_T_SLO_S = 60.0
+DEFAULT_QUEUE_ALPHA = 1.5
+EWMA_WEIGHT = 0.3
+SOLVER_DELAY_S = 0.03
+_RATE_FLOOR = 0.01
+_MAX_POINTS_PER_LAUNCH = 65535
+
+
+class PlannerError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class Plan:
+    row: object
+    workers: dict
+    batches: dict
+    lam: float
+    queues: dict
+    fidelity_cost: float
+    path_latency_s: float
+    infeasible: bool = False
+    label: str = "online"
+
+    @property
+    def total_workers(self) -> int:
+        return sum(self.workers.values())
+
+    def pair_models(self) -> list:
+        models = [self.row.light_id]
+        if self.row.heavy_id != self.row.light_id:
+            models.append(self.row.heavy_id)
+        return models
+
+    def describe(self) -> dict:
+        return {
+            "label": self.label, "light": self.row.light_id, "heavy": self.row.heavy_id,
+            "theta": self.row.theta, "tau": self.row.tau, "r_light": self.row.r_light,
+            "r_heavy": self.row.r_heavy, "workers": dict(sorted(self.workers.items())),
+            "batches": dict(sorted(self.batches.items())), "lam": self.lam,
+            "queues": dict(sorted(self.queues.items())), "fidelity_cost": self.fidelity_cost,
+            "path_latency_s": self.path_latency_s, "infeasible": self.infeasible,
+        }
+
+
+def queue_delay(queue_len: float, rate_qps: float, alpha: float = DEFAULT_QUEUE_ALPHA) -> float:
+    """Drain-time estimate for a backlog (planner.py:81-85)."""
+    if queue_len <= 0:
+        return 0.0
+    return alpha * queue_len / max(rate_qps, _RATE_FLOOR)
+
+
+def update_estimate(estimate: float, observed: float, weight: float = EWMA_WEIGHT) -> float:
+    """EWMA demand tracker (planner.py:88-90)."""
+    return weight * observed + (1.0 - weight) * estimate
+
+
+class DeviceRows:
+    """A table's rows and its catalog's latency/throughput tables in HBM.
+
+    Built once per (rows, catalog) and reused for every planning call; ``rows``
+    is any sequence of CascadeRow-like objects (ours or the reference's)."""
+
+    def __init__(self, rows, catalog, device=None):
+        torch = _lib.torch_cuda()
+        self.torch = torch
+        self.rows = tuple(rows)
+        self.catalog = catalog
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.device = dev
+        ids = [v.id for v in catalog.variants]
+        self.model_ids = ids
+        index = {m: i for i, m in enumerate(ids)}
+        bs = tuple(catalog.batch_sizes)
+        self.batch_sizes = bs
+        if not self.rows:
+            raise PlannerError("fallback: no serveable rows")
+        try:
+            rm = np.array([(index[r.light_id], index[r.heavy_id]) for r in self.rows], dtype=np.int32)
+        except KeyError as exc:
+            from .catalog import CatalogError
+            raise CatalogError(f"unknown-variant: {exc.args[0]!r}") from None
+        share = np.array([(r.r_light, r.r_heavy) for r in self.rows], dtype=np.float64)
+        fid = np.array([r.fidelity_cost for r in self.rows], dtype=np.float64)
+        variants = [catalog.by_id(m) for m in ids]
+        lat = np.array([[v.latency_s[b] for b in bs] for v in variants], dtype=np.float64)
+        mu = np.array([[v.throughput_qps[b] for b in bs] for v in variants], dtype=np.float64)
+        lat1 = np.array([v.latency_s.get(1, np.nan) for v in variants], dtype=np.float64)
+        self.d_model = torch.from_numpy(rm).to(dev)
+        self.d_share = torch.from_numpy(share).to(dev)
+        self.d_fid = torch.from_numpy(fid).to(dev)
+        self.d_batch = torch.tensor(bs, dtype=torch.int32, device=dev)
+        self.d_lat = torch.from_numpy(lat).to(dev)
+        self.d_mu = torch.from_numpy(mu).to(dev)
+        self.d_lat1 = torch.from_numpy(lat1).to(dev)
+        self._ws = None
+
+    def queue_matrix(self, queues_list):
+        q = np.zeros((len(queues_list), len(self.model_ids)), dtype=np.float64)
+        col = {m: i for i, m in enumerate(self.model_ids)}
+        for p, queues in enumerate(queues_list):
+            for m, v in (queues or {}).items():
+                if m in col:
+                    q[p, col[m]] = v
+        return q
+
+    def launch(self, lam, t_slo, workers, qmat, alpha, stream=None):
+        """Enqueue one batched solve; returns device result tensors."""
+        torch = self.torch
+        dev = self.device
+        P = int(lam.shape[0])
+        lib = _lib.load()
+        ws_bytes = lib.hadis_solve_workspace_bytes(P, len(self.rows))
+        if self._ws is None or self._ws.numel() < ws_bytes:
+            self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        out = dict(row=torch.empty(P, dtype=torch.int32, device=dev),
+                   x=torch.empty(2 * P, dtype=torch.int32, device=dev),
+                   b=torch.empty(2 * P, dtype=torch.int32, device=dev),
+                   path=torch.empty(P, dtype=torch.float64, device=dev),
+                   flags=torch.empty(P, dtype=torch.int32, device=dev))
+        p = _lib.ptr
+        _lib.check(lib.hadis_solve_many(
+            len(self.rows), p(self.d_model), p(self.d_share), p(self.d_fid), len(self.model_ids),
+            len(self.batch_sizes), p(self.d_batch), p(self.d_lat), p(self.d_mu), p(self.d_lat1), P,
+            p(lam), p(t_slo), p(workers), p(qmat), float(alpha), p(out["row"]), p(out["x"]),
+            p(out["b"]), p(out["path"]), p(out["flags"]), p(self._ws), ws_bytes,
+            _lib.stream_handle(stream)), "hadis_solve_many")
+        return out
+
+    def solve_arrays(self, lams, t_slos, workers, queues_list, alpha):
+        """Host arrays in, host result arrays out (one device round trip per chunk)."""
+        torch = self.torch
+        dev = self.device
+        lams = np.asarray(lams, dtype=np.float64)
+        t_slos = np.asarray(t_slos, dtype=np.float64)
+        workers = np.asarray(workers, dtype=np.int32)
+        qmat = self.queue_matrix(queues_list)
+        res = {k: [] for k in ("row", "x", "b", "path", "flags")}
+        for s in range(0, lams.shape[0], _MAX_POINTS_PER_LAUNCH):
+            e = min(lams.shape[0], s + _MAX_POINTS_PER_LAUNCH)
+            out = self.launch(torch.from_numpy(lams[s:e]).to(dev),
+                              torch.from_numpy(t_slos[s:e]).to(dev),
+                              torch.from_numpy(workers[s:e]).to(dev),
+                              torch.from_numpy(qmat[s:e]).to(dev), alpha)
+            for k in res:
+                res[k].append(out[k].cpu().numpy())
+        return {k: np.concatenate(v) for k, v in res.items()}
+
+
+def _plan_from(dr: DeviceRows, res, p, lam, queues, label):
+    flags = int(res["flags"][p])
+    if flags & 2:
+        raise PlannerError("solve: negative demand")
+    ri = int(res["row"][p])
+    if ri < 0:
+        raise PlannerError("fallback: no serveable rows")
+    row = dr.rows[ri]
+    infeasible = bool(flags & 1)
+    xl, xh = int(res["x"][2 * p]), int(res["x"][2 * p + 1])
+    bl, bh = int(res["b"][2 * p]), int(res["b"][2 * p + 1])
+    shares = {row.light_id: row.r_light}
+    shares[row.heavy_id] = shares.get(row.heavy_id, 0.0) + row.r_heavy
+    if row.light_id == row.heavy_id:
+        models, x, b = [row.light_id], {row.light_id: xl}, {row.light_id: bl}
+    else:
+        models = [row.light_id, row.heavy_id]
+        x = {row.light_id: xl, row.heavy_id: xh}
+        b = {row.light_id: bl, row.heavy_id: bh}
+    active = [m for m in models if shares[m] > 0]
+    # dict insertion order as the reference builds it (active models first)
+    batches = {m: b[m] for m in active}
+    for m in models:
+        batches.setdefault(m, b[m])
+    workers_map = {m: x[m] for m in models}
+    return Plan(row=row, workers=workers_map, batches=batches, lam=lam,
+                queues=dict(queues or {}), fidelity_cost=row.fidelity_cost,
+                path_latency_s=float(res["path"][p]), infeasible=infeasible, label=label)
+
+
+_CACHE: dict = {}
+
+
+def device_rows(rows, catalog) -> DeviceRows:
+    """Cached DeviceRows for a (rows, catalog) pair (rebuilt when either changes)."""
+    key = (id(rows), id(catalog))
+    hit = _CACHE.get(key)
+    if hit is not None and hit.rows == tuple(rows) and hit.catalog is catalog:
+        return hit
+    if len(_CACHE) > 32:
+        _CACHE.clear()
+    dr = DeviceRows(rows, catalog)
+    _CACHE[key] = dr
+    return dr
+
+
+def solve_many(table, catalog, lams, queues=None, workers=DEFAULT_WORKERS, t_slo=DEFAULT_T_SLO_S,
+               alpha=DEFAULT_QUEUE_ALPHA, label="online"):
+    """planner.solve for many points at once; scalars broadcast, lists are per point."""
+    lams = [float(x) for x in lams]
+    P = len(lams)
+    t_slos = [float(t_slo)] * P if np.isscalar(t_slo) else [float(x) for x in t_slo]
+    ws = [int(workers)] * P if np.isscalar(workers) else [int(x) for x in workers]
+    qs = [queues] * P if (queues is None or isinstance(queues, dict)) else list(queues)
+    rows = table.rows if hasattr(table, "rows") else table
+    dr = device_rows(rows, catalog)
+    res = dr.solve_arrays(lams, t_slos, ws, qs, alpha)
+    return [_plan_from(dr, res, p, lams[p], qs[p], label) for p in range(P)]
+
+
+def solve(table, catalog, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
+          t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA,
+          label: str = "online") -> Plan:
+    """Pick the feasible table row with the lowest fidelity cost (planner.py:217-227)."""
+    if lam < 0:
+        raise PlannerError("solve: negative demand")
+    return solve_many(table, catalog, [lam], queues, workers, t_slo, alpha, label)[0]
+
+
+def fallback_plan(indexed_rows, catalog, lam, queues, workers, t_slo, alpha, label):
+    """Overload plan over explicit (index, row) pairs (planner.py:170-214).
+
+    Runs the same device search with an SLO no plan can meet, so the
+    fallback branch decides; indices are the caller's."""
+    indexed_rows = list(indexed_rows)
+    if not indexed_rows:
+        raise PlannerError("fallback: no serveable rows")
+    rows = [r for _, r in indexed_rows]
+    order = sorted(range(len(indexed_rows)), key=lambda i: indexed_rows[i][0])
+    ordered = [rows[i] for i in order]
+    plan = solve_many(ordered, catalog, [lam], queues, workers, -float("inf"), alpha, label)[0]
+    return plan
+
+
+def make_planner(mode: str, table, catalog, workers: int = DEFAULT_WORKERS,
+                 t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA, **kwargs):
+    """(lam, queues) -> (Plan, info) callable; the GPU implements mode 'online'."""
+    if mode != "online":
+        raise PlannerError(f"mode {mode!r} is not on the accelerated path; use cascadesim's "
+                           "make_planner for the baseline planners")
+
+    def fn(lam, queues):
+        return solve(table, catalog, lam, queues, workers, t_slo, alpha), {}
+    return fn

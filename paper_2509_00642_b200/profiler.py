@@ -1,0 +1,463 @@
+"""Offline cascade profiling on the GPU: drop-in for cascadesim.profiler.
+
+Public surface (same names, signatures, return types and error behaviour as
+pkg/src/cascadesim/profiler.py):
+
+* ``THRESHOLD_GRID``, ``ProfileError``, ``CascadeRow``, ``TableProvenance``,
+  ``CascadeTable`` (profiler.py:30-98) -- field-compatible frozen dataclasses;
+* ``profile_config(catalog, prompts, seed, noise_sigma, eps_latency,
+  eps_quality, thresholds, weights)`` (profiler.py:107-186);
+* ``prompts_hash`` / ``save_table`` / ``load_table`` (profiler.py:101-104,
+  189-216), byte-identical JSON layout.
+
+Added array-level entry points (no text needed):
+
+* ``profile_records(pool_or_catalog, h, scores=None, noise=None, ...)`` --
+  the same table from per-query records (hardness, light-model scores) that
+  the reference derives from prompt text (profiler.py:125-137);
+* ``GridProfiler`` -- keeps records resident in HBM and runs the device
+  pipeline (K1 histogram, K2 scan, K3/K4 frontier) without host round trips.
+
+What runs where: text -> hardness / keyed noise stays on the host with the
+reference's own functions (the router and seeds modules of cascadesim, which
+a cascadesim user already has); scores are formed with the reference's numpy
+expression; everything from the records onward -- bypass/reject counting,
+every grid cell, the Pareto extraction and the (theta, tau) merge -- runs in
+libhadis_b200.so on the GPU.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+from . import _lib
+from .catalog import catalog_hash, select_candidates
+
+THRESHOLD_GRID = tuple(i / 10 for i in range(11))
+DEFAULT_NOISE_SIGMA = 0.05
+
+
+class ProfileError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class CascadeRow:
+    """One profiled operating point of a light/heavy cascade pair (profiler.py:37-61)."""
+
+    light_id: str
+    heavy_id: str
+    theta: float
+    tau: float
+    r_light: float
+    r_heavy: float
+    fidelity_cost: float
+    mean_latency_s: float
+
+    @property
+    def bypass_fraction(self) -> float:
+        return 1.0 - self.r_light
+
+    @property
+    def reroute_fraction(self) -> float:
+        return self.r_heavy - self.bypass_fraction
+
+    def shares(self) -> dict:
+        out = {self.light_id: self.r_light}
+        out[self.heavy_id] = out.get(self.heavy_id, 0.0) + self.r_heavy
+        return out
+
+
+@dataclass(frozen=True)
+class TableProvenance:
+    catalog_hash: str
+    prompts_hash: str
+    n_prompts: int
+    seed: int
+    noise_sigma: float
+    thresholds: tuple
+    eps_latency: float
+    eps_quality: float
+
+
+@dataclass(frozen=True)
+class CascadeTable:
+    rows: tuple
+    provenance: TableProvenance
+
+    def pairs(self) -> list:
+        seen = []
+        for row in self.rows:
+            pair = (row.light_id, row.heavy_id)
+            if pair not in seen:
+                seen.append(pair)
+        return sorted(seen)
+
+    def rows_for_pair(self, light_id: str, heavy_id: str) -> list:
+        return [r for r in self.rows if r.light_id == light_id and r.heavy_id == heavy_id]
+
+    def find_row(self, light_id, heavy_id, theta, tau) -> CascadeRow:
+        for r in self.rows_for_pair(light_id, heavy_id):
+            if abs(r.theta - theta) < 1e-12 and abs(r.tau - tau) < 1e-12:
+                return r
+        raise ProfileError(f"row-not-found: {light_id}/{heavy_id} theta={theta} tau={tau}")
+
+
+# ----------------------------------------------------------------- hashing
+
+def stable_text_key(text: str) -> int:
+    """63-bit SHA-256 prompt key (seeds.py:49-55)."""
+    return int.from_bytes(hashlib.sha256(text.encode("utf-8")).digest()[:8], "big") >> 1
+
+
+def prompts_hash(prompts) -> str:
+    """Order-free hash of a prompt population (profiler.py:101-104)."""
+    blob = "\x1f".join(sorted(prompts, key=stable_text_key)).encode("utf-8")
+    return hashlib.sha256(blob).hexdigest()[:16]
+
+
+# ------------------------------------------------------------- table I/O
+
+def save_table(table: CascadeTable, path: str) -> None:
+    """JSON layout of profiler.py:189-196 (indent=1, sort_keys, trailing newline)."""
+    doc = {"provenance": asdict(table.provenance), "rows": [asdict(r) for r in table.rows]}
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(doc, fh, indent=1, sort_keys=True)
+        fh.write("\n")
+
+
+def load_table(path: str, catalog=None, override_provenance: bool = False) -> CascadeTable:
+    """Reader with the provenance gate of profiler.py:199-216."""
+    with open(path, "r", encoding="utf-8") as fh:
+        doc = json.load(fh)
+    try:
+        prov = dict(doc["provenance"])
+        prov["thresholds"] = tuple(prov["thresholds"])
+        provenance = TableProvenance(**prov)
+        rows = tuple(CascadeRow(**r) for r in doc["rows"])
+    except (KeyError, TypeError) as exc:
+        raise ProfileError(f"table file: malformed ({exc})") from None
+    if catalog is not None:
+        current = catalog_hash(catalog)
+        if provenance.catalog_hash != current and not override_provenance:
+            raise ProfileError(
+                "provenance-mismatch: table was profiled against catalog "
+                f"{provenance.catalog_hash}, current catalog is {current}; "
+                "pass override_provenance to use it anyway")
+    return CascadeTable(rows=rows, provenance=provenance)
+
+
+# ------------------------------------------------------ grid description
+
+def _light_first(v):
+    return (v.latency_s[1], v.id)
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Threshold list as given plus its sorted distinct values.
+
+    ``first_pos[r]`` is the first position of the r-th smallest distinct
+    value -- the representative the reference's index tie-break keeps."""
+
+    thresholds: tuple
+    unique: tuple
+    first_pos: tuple
+
+    @staticmethod
+    def build(thresholds) -> "GridSpec":
+        thr = tuple(float(t) for t in thresholds)
+        if not thr:
+            raise ProfileError("profile_config: empty threshold grid")
+        if any(math.isnan(t) for t in thr):
+            raise ProfileError("profile_config: NaN thresholds are not supported")
+        first = {}
+        for i, t in enumerate(thr):
+            first.setdefault(t, i)   # -0.0 and 0.0 share one key, as in the reference's dict
+        uniq = tuple(sorted(first))
+        return GridSpec(thr, uniq, tuple(first[u] for u in uniq))
+
+
+def light_scores(pool, h, noise):
+    """Discriminator scores of every light-capable pool model (profiler.py:134-137),
+    rows in pool latency order (the heaviest model is never a light stage)."""
+    h = np.asarray(h, dtype=np.float64)
+    noise = np.asarray(noise, dtype=np.float64)
+    out = np.empty((len(pool) - 1, h.shape[0]), dtype=np.float64)
+    for i, v in enumerate(pool[:-1]):
+        a, s = v.accept_params
+        out[i] = np.clip(1.0 / (1.0 + np.exp(-(a - s * h))) + noise, 0.0, 1.0)
+    return out
+
+
+def pair_list(pool):
+    return [(i, j) for i in range(len(pool)) for j in range(i + 1, len(pool))]
+
+
+def pair_params(pool, pairs):
+    rows = []
+    for i, j in pairs:
+        lt, hv = pool[i], pool[j]
+        rows.append((lt.latency_s[1], hv.latency_s[1], lt.base_quality_cost, lt.hardness_penalty,
+                     hv.base_quality_cost, hv.hardness_penalty))
+    return np.asarray(rows, dtype=np.float64).reshape(len(pairs), _lib.PAIR_PARAMS)
+
+
+# --------------------------------------------------------- device pipeline
+
+@dataclass
+class DeviceTable:
+    """Raw device output of one profiling run (rows in pair-major (theta, tau) order)."""
+
+    pairs: list          # (light pool index, heavy pool index) per local pair id
+    n_rows: int
+    pair_rows: list      # rows per local pair
+    pair: object         # torch int32 [rows]
+    theta_pos: object
+    tau_pos: object
+    r_light: object      # torch float64 [rows]
+    r_heavy: object
+    fid: object
+    lat: object
+    stats: dict
+
+
+class GridProfiler:
+    """Records resident in HBM + the K1..K4 device pipeline.
+
+    ``h`` is float64[N] and ``scores`` float64[L, N] (row i = pool model i as
+    the light stage), both in ``stable_text_key`` order and already on the
+    device (torch tensors) or host arrays copied once at construction."""
+
+    def __init__(self, pool, h, scores, device=None):
+        torch = _lib.torch_cuda()
+        self.torch = torch
+        self.pool = list(pool)
+        if len(self.pool) < 2:
+            raise ProfileError("profile_config: need at least two candidate variants")
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.h = torch.as_tensor(h, dtype=torch.float64, device=self.device).contiguous()
+        self.scores = torch.as_tensor(scores, dtype=torch.float64, device=self.device).contiguous()
+        self.n = int(self.h.shape[0])
+        if self.n == 0:
+            raise ProfileError("profile_config: empty prompt population")
+        if self.scores.dim() != 2 or self.scores.shape[1] != self.n or \
+                self.scores.shape[0] < len(self.pool) - 1:
+            raise ProfileError("profile_records: scores must be [n_models - 1, n_records]")
+        self.lib = _lib.load()
+        self.shift = self.lib.hadis_hfix_shift(self.n)
+        self._ws = None
+        self._caps = None
+
+    # -- K1 + K2 ---------------------------------------------------------
+    def histograms(self, grid: GridSpec, slot0: int, n_light: int, stream=None):
+        torch = self.torch
+        U = len(grid.unique)
+        bins = (U + 1) * (U + 1) * n_light
+        cnt = torch.empty(bins, dtype=torch.int32, device=self.device)
+        hsum = torch.empty(bins, dtype=torch.int64, device=self.device)
+        bad = torch.empty(1, dtype=torch.int32, device=self.device)
+        d_u = torch.tensor(grid.unique, dtype=torch.float64, device=self.device)
+        st = _lib.stream_handle(stream)
+        scores = self.scores[slot0:slot0 + n_light]
+        _lib.check(self.lib.hadis_bin_hist(_lib.ptr(self.h), _lib.ptr(scores), self.n, n_light,
+                                           _lib.ptr(d_u), U, self.shift, _lib.ptr(cnt),
+                                           _lib.ptr(hsum), _lib.ptr(bad), st), "hadis_bin_hist")
+        _lib.check(self.lib.hadis_hist_scan(_lib.ptr(cnt), _lib.ptr(hsum), n_light, U, st),
+                   "hadis_hist_scan")
+        return cnt, hsum, bad, d_u
+
+    # -- K3 + K4 ---------------------------------------------------------
+    def run(self, thresholds=THRESHOLD_GRID, pairs=None, exact_fid=False, stream=None,
+            caps=None, sync=True):
+        """Profile ``pairs`` (default: all light<heavy pairs).  Returns a DeviceTable.
+
+        With ``sync=False`` nothing waits for the device: the caller must call
+        ``finish(...)`` (which synchronises) before reading results."""
+        torch = self.torch
+        grid = GridSpec.build(thresholds)
+        pairs = pair_list(self.pool) if pairs is None else list(pairs)
+        if not pairs:
+            raise ProfileError("profile_records: no pairs to profile")
+        U = len(grid.unique)
+        slots = sorted({i for i, _ in pairs})
+        slot0, n_light = slots[0], slots[-1] - slots[0] + 1
+        cnt, hsum, bad, d_u = self.histograms(grid, slot0, n_light, stream)
+        d_slot = torch.tensor([i - slot0 for i, _ in pairs], dtype=torch.int32, device=self.device)
+        d_params = torch.from_numpy(pair_params(self.pool, pairs)).to(self.device)
+        d_first = torch.tensor(grid.first_pos, dtype=torch.int32, device=self.device)
+        scores = self.scores[slot0:slot0 + n_light]
+        P = len(pairs)
+        if caps is None:
+            cells = U * U * P
+            cand = int(min(cells, max(1 << 20, cells // 8)))
+            caps = (cand, 2048, int(min(cells, cand + U * P)))
+        state = dict(grid=grid, pairs=pairs, cnt=cnt, hsum=hsum, bad=bad, d_u=d_u, d_slot=d_slot,
+                     d_params=d_params, d_first=d_first, scores=scores, exact_fid=exact_fid,
+                     stream=stream)
+        self._launch(state, caps)
+        if not sync:
+            return state
+        return self.finish(state)
+
+    def _launch(self, state, caps):
+        torch = self.torch
+        cand_cap, exact_cap, out_cap = caps
+        grid, pairs = state["grid"], state["pairs"]
+        U, P = len(grid.unique), len(pairs)
+        ws_bytes = self.lib.hadis_frontier_workspace_bytes(P, U, cand_cap, exact_cap, out_cap)
+        if ws_bytes == 0:
+            raise ProfileError("profile_records: invalid frontier sizes")
+        if self._ws is None or self._ws.numel() < ws_bytes:
+            self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        dev = self.device
+        out = dict(pair=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                   theta_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                   tau_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                   r_light=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                   r_heavy=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                   fid=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                   lat=torch.empty(out_cap, dtype=torch.float64, device=dev))
+        stats = torch.zeros(_lib.ST_PAIR0 + P, dtype=torch.int64, device=dev)
+        p = _lib.ptr
+        _lib.check(self.lib.hadis_pair_frontiers(
+            p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(state["d_slot"]),
+            p(state["d_params"]), p(state["d_first"]), len(grid.thresholds), p(state["d_u"]),
+            p(self.h), p(state["scores"]), 1 if state["exact_fid"] else 0, p(self._ws), ws_bytes,
+            cand_cap, exact_cap, out_cap, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]),
+            p(out["r_light"]), p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
+            _lib.stream_handle(state["stream"])), "hadis_pair_frontiers")
+        state.update(out=out, stats=stats, caps=caps)
+
+    def finish(self, state) -> DeviceTable:
+        """Synchronise, check device-side status, grow capacities and rerun if needed."""
+        for _ in range(6):
+            stats = state["stats"].cpu().tolist()
+            if int(state["bad"].item()):
+                raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
+            if stats[_lib.ST_OVERFLOW] == 0:
+                break
+            cand_cap, exact_cap, out_cap = state["caps"]
+            U, P = len(state["grid"].unique), len(state["pairs"])
+            cells = U * U * P
+            cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
+            out_cap = int(min(cells, max(out_cap * 2, cand_cap + U * P)))
+            if stats[_lib.ST_OVERFLOW] & (2 | 4 | 64):
+                raise ProfileError("profile_records: too many exactness-critical cells "
+                                   f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
+            self._launch(state, (cand_cap, exact_cap, out_cap))
+        else:
+            raise ProfileError("profile_records: capacity retries exhausted")
+        n_rows = stats[_lib.ST_ROWS]
+        out = state["out"]
+        return DeviceTable(
+            pairs=state["pairs"], n_rows=n_rows,
+            pair_rows=stats[_lib.ST_PAIR0:_lib.ST_PAIR0 + len(state["pairs"])],
+            pair=out["pair"][:n_rows], theta_pos=out["theta_pos"][:n_rows],
+            tau_pos=out["tau_pos"][:n_rows], r_light=out["r_light"][:n_rows],
+            r_heavy=out["r_heavy"][:n_rows], fid=out["fid"][:n_rows], lat=out["lat"][:n_rows],
+            stats={"rows": n_rows, "candidates": stats[_lib.ST_CANDIDATES],
+                   "uncertain": stats[_lib.ST_UNCERTAIN],
+                   "exact_cells": stats[_lib.ST_EXACT_CELLS]})
+
+
+def rows_from_device(dt: DeviceTable, pool, thresholds) -> tuple:
+    """Materialise CascadeRow objects (host) from a DeviceTable."""
+    thr = tuple(float(t) for t in thresholds)
+    pair = dt.pair.cpu().numpy()
+    th = dt.theta_pos.cpu().numpy()
+    ta = dt.tau_pos.cpu().numpy()
+    rl = dt.r_light.cpu().numpy().tolist()
+    rh = dt.r_heavy.cpu().numpy().tolist()
+    fid = dt.fid.cpu().numpy().tolist()
+    lat = dt.lat.cpu().numpy().tolist()
+    ids = [(pool[i].id, pool[j].id) for i, j in dt.pairs]
+    return tuple(CascadeRow(light_id=ids[p][0], heavy_id=ids[p][1], theta=thr[a], tau=thr[b],
+                            r_light=x1, r_heavy=x2, fidelity_cost=f, mean_latency_s=m)
+                 for p, a, b, x1, x2, f, m in zip(pair.tolist(), th.tolist(), ta.tolist(), rl, rh,
+                                                  fid, lat))
+
+
+def _pool_of(pool_or_catalog, eps_latency, eps_quality):
+    if hasattr(pool_or_catalog, "variants"):
+        pool = select_candidates(pool_or_catalog, eps_latency, eps_quality)
+    else:
+        pool = sorted(pool_or_catalog, key=_light_first)
+    if len(pool) < 2:
+        raise ProfileError("profile_config: need at least two candidate variants")
+    return pool
+
+
+def profile_records(pool_or_catalog, h, scores=None, noise=None, thresholds=THRESHOLD_GRID,
+                    eps_latency=0.1, eps_quality=0.1, exact_fid=False, provenance=None):
+    """CascadeTable from per-query records (array-level profile_config).
+
+    ``h``: hardness in [0, 1] per query; ``scores``: dict model id -> float64[N]
+    or an array [n_pool - 1, N] (pool latency order); or ``noise`` to derive
+    scores exactly as profiler.py:134-137.  Records must be in the order the
+    reference would use (``stable_text_key`` order of the prompts) for
+    ``exact_fid`` to be bitwise-identical; counts, latencies and membership do
+    not depend on order."""
+    pool = _pool_of(pool_or_catalog, eps_latency, eps_quality)
+    h = np.asarray(h, dtype=np.float64) if not hasattr(h, "is_cuda") else h
+    if h.shape[0] == 0:
+        raise ProfileError("profile_config: empty prompt population")
+    if scores is None:
+        if noise is None:
+            raise ProfileError("profile_records: give scores or noise")
+        scores = light_scores(pool, h, noise)
+    elif isinstance(scores, dict):
+        scores = np.stack([np.asarray(scores[v.id], dtype=np.float64) for v in pool[:-1]])
+    prof = GridProfiler(pool, h, scores)
+    dt = prof.run(thresholds, exact_fid=exact_fid)
+    rows = rows_from_device(dt, pool, thresholds)
+    if provenance is None:
+        cat = pool_or_catalog if hasattr(pool_or_catalog, "variants") else None
+        provenance = TableProvenance(
+            catalog_hash=catalog_hash(cat) if cat is not None else "",
+            prompts_hash="", n_prompts=prof.n, seed=0, noise_sigma=0.0,
+            thresholds=tuple(float(t) for t in thresholds), eps_latency=eps_latency,
+            eps_quality=eps_quality)
+    return CascadeTable(rows=rows, provenance=provenance)
+
+
+def _text_records(texts, seed, noise_sigma, weights):
+    """Hardness + keyed noise per prompt with the reference's own host functions."""
+    try:
+        from cascadesim import router
+        from cascadesim.seeds import stream_normal
+    except ImportError as exc:  # pragma: no cover - depends on the user's install
+        raise ImportError("profile_config on prompt text needs cascadesim's router/seeds "
+                          "(text -> hardness); use profile_records with precomputed "
+                          "records otherwise") from exc
+    lex = router.load_lexicons()
+    h = np.array([router.hardness(t, weights, lex) for t in texts], dtype=np.float64)
+    noise = np.array([stream_normal(seed, stable_text_key(t), "disc", sigma=noise_sigma)
+                      for t in texts], dtype=np.float64)
+    return h, noise
+
+
+def profile_config(catalog, prompts, seed: int = 0, noise_sigma: float = DEFAULT_NOISE_SIGMA,
+                   eps_latency: float = 0.1, eps_quality: float = 0.1,
+                   thresholds=THRESHOLD_GRID, weights=None, exact_fid: bool = True) -> CascadeTable:
+    """Drop-in for cascadesim.profiler.profile_config (profiler.py:107-186).
+
+    ``exact_fid`` (default True) recomputes every emitted row's fidelity with
+    the numpy-exact emulation so the returned table equals the reference's
+    bit for bit; False keeps the fixed-point fidelity (within ~1e-12 relative)."""
+    if not prompts:
+        raise ProfileError("profile_config: empty prompt population")
+    pool = _pool_of(catalog, eps_latency, eps_quality)
+    thr = tuple(float(t) for t in thresholds)
+    texts = sorted(prompts, key=stable_text_key)
+    h, noise = _text_records(texts, seed, noise_sigma, weights)
+    prov = TableProvenance(catalog_hash=catalog_hash(catalog), prompts_hash=prompts_hash(texts),
+                           n_prompts=len(texts), seed=seed, noise_sigma=noise_sigma,
+                           thresholds=thr, eps_latency=eps_latency, eps_quality=eps_quality)
+    return profile_records(pool, h, scores=light_scores(pool, h, noise), thresholds=thr,
+                           exact_fid=exact_fid, provenance=prov)

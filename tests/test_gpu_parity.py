@@ -1,0 +1,252 @@
+"""GPU parity: libhadis_b200 vs the reference (golden fixtures) and the oracle.
+
+Every test here runs the CUDA path through the C ABI (via the package's
+ctypes layer) and compares with the reference's own outputs or with the CPU
+oracle on the same seeded inputs."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+from oracle import grid as og
+from oracle import planner as op
+from paper_2509_00642_b200 import (GridProfiler, default_catalog, pareto_prune, profile_records,
+                                   solve, solve_many)
+from paper_2509_00642_b200.catalog import select_candidates
+from paper_2509_00642_b200.planner import PlannerError
+from paper_2509_00642_b200.profiler import GridSpec, light_scores
+from tests.goldens import (PROFILE_CASES, catalog_from_doc, load_json, load_npz, row_tuples,
+                           rows_ns, scores_of)
+
+pytestmark = pytest.mark.gpu
+
+
+def tuples(table):
+    return [(r.light_id, r.heavy_id, r.theta, r.tau, r.r_light, r.r_heavy, r.fidelity_cost,
+             r.mean_latency_s) for r in table.rows]
+
+
+def assert_rows_close(got, want, rel=1e-9):
+    """Identical membership/order, bit-exact counts-derived fields, fid within rel."""
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g[:6] == w[:6] and g[7] == w[7], (g, w)
+        assert math.isclose(g[6], w[6], rel_tol=rel, abs_tol=0.0), (g, w)
+
+
+def _golden_pool(doc):
+    cat = catalog_from_doc(doc["catalog"])
+    return cat, select_candidates(cat, doc["eps"], doc["eps"])
+
+
+@pytest.mark.parametrize("variant", ["default", "bypass01", "unsorted", "duplicates", "negzero",
+                                     "dense33"])
+@pytest.mark.parametrize("exact", [True, False])
+def test_conftest160_matches_reference(gpu_device, variant, exact):
+    doc = load_json("conftest160")
+    rec = load_npz("conftest160")
+    cat, pool = _golden_pool(doc)
+    case = doc["variants"][variant]
+    table = profile_records(cat, rec["h"], scores=scores_of(rec), thresholds=case["thresholds"],
+                            exact_fid=exact)
+    want = row_tuples(case["table"])
+    if exact:
+        assert tuples(table) == want
+    else:
+        assert_rows_close(tuples(table), want)
+
+
+@pytest.mark.parametrize("name", ("c1",) + PROFILE_CASES)
+@pytest.mark.parametrize("exact", [True, False])
+def test_golden_profiles_match_reference(gpu_device, name, exact):
+    doc = load_json(name)
+    rec = load_npz(name)
+    cat, pool = _golden_pool(doc)
+    table = profile_records(cat, rec["h"], scores=scores_of(rec), thresholds=doc["thresholds"],
+                            eps_latency=doc["eps"], eps_quality=doc["eps"], exact_fid=exact)
+    want = row_tuples(doc["table"])
+    if exact:
+        assert tuples(table) == want
+    else:
+        assert_rows_close(tuples(table), want)
+
+
+@pytest.mark.parametrize("seed,n,k,hmode", [(1, 1, 5, "u"), (2, 7, 9, "u"), (3, 300, 17, "ties"),
+                                            (4, 1000, 40, "u"), (5, 4000, 64, "ties"),
+                                            (6, 2500, 33, "clip"), (7, 129, 128, "u")])
+def test_random_records_match_oracle(gpu_device, seed, n, k, hmode):
+    rng = np.random.default_rng(seed)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    if hmode == "ties":
+        h = rng.choice(np.round(rng.uniform(0.0, 1.0, 37), 2), n)
+    else:
+        h = rng.uniform(0.0, 1.0, n)
+    sigma = 0.3 if hmode == "clip" else 0.05
+    noise = rng.normal(0.0, sigma, n)
+    thr = tuple(rng.permutation(np.linspace(0.0, 1.0, k)).tolist())
+    want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
+    got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
+    assert tuples(got) == want
+    got2 = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=False)
+    assert_rows_close(tuples(got2), want)
+
+
+def test_fid_exact_kernel_is_numpy(gpu_device):
+    import torch
+    from paper_2509_00642_b200 import _lib
+    rng = np.random.default_rng(3)
+    lib = _lib.load()
+    for n in (1, 5, 8, 127, 128, 129, 1000, 4099, 65537, 1000003):
+        h = rng.uniform(0, 1, n)
+        s = rng.uniform(0, 1, (2, n))
+        cells = [(0, 0.3, 0.5, 30.0, 8.0, 25.0, 3.0), (1, 0.0, 1.0, 36.0, 12.0, 23.0, 3.0),
+                 (1, 0.7, 0.2, 31.0, 8.0, 26.0, 5.0)]
+        dev = torch.device("cuda")
+        d_h = torch.from_numpy(h).to(dev)
+        d_s = torch.from_numpy(s).to(dev)
+        slot = torch.tensor([c[0] for c in cells], dtype=torch.int32, device=dev)
+        th = torch.tensor([c[1] for c in cells], dtype=torch.float64, device=dev)
+        ta = torch.tensor([c[2] for c in cells], dtype=torch.float64, device=dev)
+        par = torch.tensor([c[3:] for c in cells], dtype=torch.float64, device=dev)
+        out = torch.empty(len(cells), dtype=torch.float64, device=dev)
+        _lib.check(lib.hadis_fid_exact(_lib.ptr(d_h), _lib.ptr(d_s), n, len(cells), _lib.ptr(slot),
+                                       _lib.ptr(th), _lib.ptr(ta), _lib.ptr(par), _lib.ptr(out),
+                                       _lib.stream_handle()), "fid_exact")
+        got = out.cpu().tolist()
+        for c, g in zip(cells, got):
+            heavy = (h > c[1]) | (s[c[0]] < c[2])
+            want = float(np.where(heavy, c[5] + c[6] * h, c[3] + c[4] * h).mean())
+            assert g == want, (n, c)
+
+
+def test_pareto_prune_kats(gpu_device):
+    for case in load_json("pareto_kats")["cases"]:
+        rows = [tuple(r) + (i,) for i, r in enumerate(case["rows"])]
+        kept = pareto_prune(rows, key=lambda r: (r[0], r[1]))
+        assert [r[2] for r in kept] == case["kept"]
+    assert pareto_prune([(1.0, 5.0), (2.0, 4.0), (1.5, 6.0)]) == [(1.0, 5.0), (2.0, 4.0)]
+    assert pareto_prune([]) == []
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 100, 2047, 2048, 2049, 5000, 70001])
+def test_pareto_prune_random(gpu_device, n):
+    rng = random.Random(n)
+    rows = [(rng.choice([0.5, 1.0, rng.uniform(0, 10)]), rng.choice([1.0, rng.uniform(0, 10)]))
+            for _ in range(n)]
+    got = pareto_prune(rows)
+    want = [rows[i] for i in og.pareto_keep([r[0] for r in rows], [r[1] for r in rows])]
+    assert got == want
+
+
+def _plan_matches(plan, want, rows):
+    assert plan.row == rows[want["row_index"]]
+    assert plan.workers == want["workers"]
+    assert plan.batches == want["batches"]
+    assert plan.path_latency_s == want["path_latency_s"]
+    assert plan.fidelity_cost == want["fidelity_cost"]
+    assert plan.infeasible == want["infeasible"]
+
+
+def test_planner_random200_matches_reference(gpu_device):
+    cases = load_json("planner_random200")["cases"]
+    for case in cases:
+        cat = catalog_from_doc(case["catalog"])
+        rows = rows_ns(case["rows"])
+        try:
+            plan = solve(rows, cat, case["lam"], case["queues"], case["workers"], case["t_slo"],
+                         case["alpha"])
+        except PlannerError as exc:
+            assert case["solve"] is None and case["solve_error"] == str(exc)
+            continue
+        _plan_matches(plan, case["solve"], rows)
+
+
+def test_planner_conftest_sweep_matches_reference(gpu_device):
+    doc = load_json("planner_conftest")
+    cat = catalog_from_doc(doc["catalog"])
+    rows = rows_ns(doc["table"]["rows"])
+    pts = doc["points"]
+    plans = solve_many(rows, cat, [p["lam"] for p in pts], [p["queues"] for p in pts],
+                       [p["workers"] for p in pts], [p["t_slo"] for p in pts], 1.5)
+    for plan, pt in zip(plans, pts):
+        _plan_matches(plan, pt["solve"], rows)
+
+
+def test_planner_errors(gpu_device):
+    doc = load_json("planner_conftest")
+    cat = catalog_from_doc(doc["catalog"])
+    rows = rows_ns(doc["table"]["rows"])
+    with pytest.raises(PlannerError, match="negative demand"):
+        solve(rows, cat, -1.0)
+    dead = rows_ns([dict(doc["table"]["rows"][0], r_light=0.0, r_heavy=0.0)])
+    # a row with no load is trivially feasible (zero workers), as in the reference
+    plan = solve(dead, cat, 3.0)
+    want = op.solve(dead, cat, 3.0)
+    _plan_matches(plan, want, dead)
+    # ... but when nothing meets the SLO the fallback has no serveable row
+    with pytest.raises(PlannerError, match="no serveable rows"):
+        solve(dead, cat, 3.0, t_slo=0.01)
+    with pytest.raises(op.OraclePlannerError, match="no serveable rows"):
+        op.solve(dead, cat, 3.0, t_slo=0.01)
+
+
+def test_planner_sweep_vs_oracle_on_gpu_table(gpu_device):
+    rng = np.random.default_rng(11)
+    cat = default_catalog()
+    h = rng.uniform(0.05, 0.9, 20000)
+    noise = rng.normal(0, 0.05, 20000)
+    table = profile_records(cat, h, noise=noise, thresholds=tuple(i / 31 for i in range(32)))
+    pr = random.Random(5)
+    lams = [pr.uniform(0, 120) for _ in range(60)] + [0.0]
+    ts = [pr.choice([5.0, 15.0, 30.0, 60.0, 90.0]) for _ in lams]
+    ws = [pr.choice([1, 2, 3, 8, 16]) for _ in lams]
+    qs = [({m: pr.uniform(0, 40) for m in cat.ids() if pr.random() < 0.5} if pr.random() < 0.5
+           else {}) for _ in lams]
+    plans = solve_many(table, cat, lams, qs, ws, ts, 1.5)
+    for plan, lam, t, w, q in zip(plans, lams, ts, ws, qs):
+        want = op.solve(table.rows, cat, lam, q, w, t, 1.5)
+        _plan_matches(plan, want, table.rows)
+
+
+@pytest.mark.slow
+def test_c2_scale_properties(gpu_device):
+    """c2 shape (4 models, 1M records, 256 thresholds): size-independent checks."""
+    rng = np.random.default_rng(20261017)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    n = 1_000_000
+    h = rng.uniform(0.05, 0.9, n)
+    noise = rng.normal(0.0, 0.05, n)
+    thr = tuple(i / 255 for i in range(256))
+    scores = light_scores(pool, h, noise)
+    prof = GridProfiler(pool, h, scores)
+    dt = prof.run(thr)
+    from paper_2509_00642_b200.profiler import rows_from_device
+    rows = rows_from_device(dt, pool, thr)
+    assert len(rows) == dt.n_rows > 0
+    by_pair = {}
+    for r in rows:
+        by_pair.setdefault((r.light_id, r.heavy_id), []).append(r)
+    assert len(by_pair) == 6
+    for prs in by_pair.values():
+        keys = [(r.theta, r.tau) for r in prs]
+        assert keys == sorted(keys)
+        for a in prs:     # frontier property (profiler tests: test_rows_per_pair_form_frontier)
+            for b in prs:
+                if a is b:
+                    continue
+                dom = (b.mean_latency_s <= a.mean_latency_s and b.fidelity_cost <= a.fidelity_cost
+                       and (b.mean_latency_s < a.mean_latency_s or b.fidelity_cost < a.fidelity_cost))
+                assert not dom or a.theta == 1.0
+    # bit-exact counts / latency and 1e-9 fidelity on a sample of rows, via numpy
+    cost, sc = og.model_arrays(pool, h, noise)
+    ids = {v.id: v for v in pool}
+    for r in random.Random(1).sample(rows, 12):
+        lt, hv = ids[r.light_id], ids[r.heavy_id]
+        nb, nr, rl, rh, fid, lat = og.cell_stats(h, sc[lt.id], cost[lt.id], cost[hv.id],
+                                                 lt.latency_s[1], hv.latency_s[1], r.theta, r.tau)
+        assert (r.r_light, r.r_heavy, r.mean_latency_s) == (rl, rh, lat)
+        assert math.isclose(r.fidelity_cost, fid, rel_tol=1e-9)
