@@ -46,6 +46,8 @@ enum hadis_status {
 int hadis_abi_version(void);
 const char* hadis_status_string(int status);
 const char* hadis_last_cuda_error(void);
+/* Number of CUDA kernels this library has launched in the process (monotone). */
+int64_t hadis_kernel_launches(void);
 
 /* ------------------------------------------------------------------------- */
 /* Profiling: grid evaluator + Pareto extractor                               */

@@ -28,6 +28,7 @@ _SIGNATURES = {
     "hadis_abi_version": (_c_int, []),
     "hadis_status_string": (ctypes.c_char_p, [_c_int]),
     "hadis_last_cuda_error": (ctypes.c_char_p, []),
+    "hadis_kernel_launches": (_c_i64, []),
     "hadis_hfix_shift": (_c_int, [_c_i64]),
     "hadis_bin_hist": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp,
                                 _c_vp, _c_vp]),

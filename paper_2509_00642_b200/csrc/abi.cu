@@ -3,7 +3,14 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 static thread_local char g_last_cuda_error[256] = "";
+static std::atomic<long long> g_launches{0};
+
+void hadis_count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+extern "C" int64_t hadis_kernel_launches(void) { return g_launches.load(); }
 
 void hadis_set_cuda_error(cudaError_t e) {
   std::strncpy(g_last_cuda_error, cudaGetErrorString(e), sizeof(g_last_cuda_error) - 1);

@@ -20,6 +20,7 @@
 #define HADIS_LAUNCH_CHECK() HADIS_CUDA_TRY(cudaGetLastError())
 
 void hadis_set_cuda_error(cudaError_t e);
+void hadis_count_launches(int k);  // bookkeeping for hadis_kernel_launches()
 
 namespace hadis {
 

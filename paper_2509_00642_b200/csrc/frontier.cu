@@ -37,8 +37,9 @@ enum : uint32_t { kKept = 1u, kUncertain = 2u };
 
 struct PairConst {
   double Ll, Lh, bl, pl, bh, ph;
-  double delta2;     // 2 * delta
-  double lo, scale;  // latency bucket map
+  double delta2;       // 2 * delta (fidelity space)
+  double delta2_S;     // the same margin in numerator space (fid* * n), padded
+  double lo_x, scale_x;  // latency-numerator bucket map: b = floor((x - lo_x) * scale_x)
   int slot;
 };
 
@@ -52,6 +53,9 @@ struct Grid {
   int K;
   const int32_t* first_pos;
   int64_t bm_stride;        // bits per pair in the kept bitmap (words_per_pair * 32)
+  const int32_t* pk;        // twin row: largest k' < k with R[k'] < R[k], else -1
+  const int32_t* row_rep;   // rank with the smallest first_pos in k's row class
+  const uint8_t* row_start; // 1 if k starts its row class (R[k-1] < R[k])
 };
 
 struct CellVal {
@@ -92,11 +96,65 @@ __device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc,
   return v;
 }
 
-__device__ __forceinline__ int bucket_of(const PairConst& pc, int nbuckets, double lat) {
-  double x = floor(__dmul_rn(__dadd_rn(lat, -pc.lo), pc.scale));
-  if (!(x >= 0.0)) x = 0.0;
-  if (x > (double)(nbuckets - 1)) x = (double)(nbuckets - 1);
-  return (int)x;
+// Division-free numerators: x = (n-nb) L_i + (nb+nr) L_j  (lat = x / n) and
+// S = fid* * n.  Both are monotone images of lat / fid*, enough to bucket and filter.
+__device__ __forceinline__ void cell_numerators(const Grid& g, const PairConst& pc, int k, int t,
+                                                double* x, double* S) {
+  const uint32_t* C = slot_cnt(g, pc.slot);
+  const uint64_t* Sh = slot_hs(g, pc.slot);
+  const int64_t rk = (int64_t)k * g.B1;
+  const uint32_t Rk = C[rk + g.U];
+  const uint64_t Htot = Sh[(int64_t)g.U * g.B1 + g.U];
+  const uint32_t n = (uint32_t)g.n;
+  const uint32_t nH = (n - Rk) + C[rk + t];
+  const uint64_t SH = (Htot - Sh[rk + g.U]) + Sh[rk + t];
+  const uint64_t SL = Htot - SH;
+  *x = __dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh));
+  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)SH), __dmul_rn(pc.pl, (double)SL)),
+                                 g.inv_scale);
+  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, (double)nH), __dmul_rn(pc.bl, (double)(n - nH))), hterm);
+}
+
+// bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
+__device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, double x) {
+  double b = floor(__dmul_rn(__dadd_rn(x, -pc.lo_x), pc.scale_x));
+  if (!(b >= 0.0)) b = 0.0;
+  if (b > (double)(nbuckets - 1)) b = (double)(nbuckets - 1);
+  return (int)b;
+}
+
+__device__ __forceinline__ int bucket_of(const Grid& g, const PairConst& pc, int k, int t) {
+  double x, S;
+  cell_numerators(g, pc, k, t, &x, &S);
+  return bucket_of_x(pc, g.nbuckets, x);
+}
+
+// Is (k, t) the first cell of its exact-duplicate class?  Classes are
+// rectangles {row class of k} x {run of equal reject counts along tau}.
+__device__ __forceinline__ bool class_start(const Grid& g, const uint32_t* C, int k, int t) {
+  if (!g.row_start[k]) return false;
+  const int64_t rk = (int64_t)k * g.B1;
+  return t == 0 || C[rk + t] != C[rk + t - 1];
+}
+
+// Rank with the smallest first position in the tau-run of row k containing t.
+__device__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t) {
+  const uint32_t* row = C + (int64_t)k * g.B1;
+  const uint32_t v = row[t];
+  int lo = 0, hi = t;                         // first index with row[idx] == v
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (row[mid] < v) lo = mid + 1; else hi = mid; }
+  const int start = lo;
+  lo = t + 1; hi = g.U;                       // first index with row[idx] > v
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (row[mid] <= v) lo = mid + 1; else hi = mid; }
+  int best = start;
+  for (int i = start + 1; i < lo; ++i)
+    if (g.first_pos[i] < g.first_pos[best]) best = i;
+  return best;
+}
+
+// representative (smallest grid index) cell of (k, t)'s duplicate class
+__device__ __forceinline__ uint32_t rep_cell(const Grid& g, const uint32_t* C, int k, int t) {
+  return (uint32_t)(g.row_rep[k] * g.U + rep_tau(g, C, k, t));
 }
 
 __device__ __forceinline__ int64_t grid_index(const Grid& g, int k, int t) {
@@ -135,24 +193,39 @@ __global__ void pair_const_kernel(int n_pairs, const int32_t* __restrict__ pair_
   const double pmax = fmax(fabs(c.pl), fabs(c.ph));
   const double delta = 2.0 * (128.0 * u * fbig + pmax * ldexp(1.0, -shift)) + DBL_MIN;
   c.delta2 = 2.0 * delta;
-  const double lo = fmin(c.Ll, c.Lh) * (1.0 - 1e-12);
-  const double hi = (c.Ll + c.Lh) * (1.0 + 1e-12);
-  c.lo = lo;
-  c.scale = (double)nbuckets / (hi - lo);
-  (void)n;
+  const double dn = (double)n;
+  c.delta2_S = c.delta2 * dn * 1.001;
+  const double lo = fmin(c.Ll, c.Lh) * dn * (1.0 - 1e-12);
+  const double hi = (c.Ll + c.Lh) * dn * (1.0 + 1e-12);
+  c.lo_x = lo;
+  c.scale_x = (double)nbuckets / (hi - lo);
   out[p] = c;
 }
 
-// pk[k] = largest k' < k with R[k'] < R[k] (else -1): canonical heavy-set twin row
-__global__ void twin_row_kernel(const uint32_t* __restrict__ cnt, int U, int B1, int32_t* pk) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  int last = -1;         // last rank whose R differs from the run that follows
-  uint32_t prevR = 0;
-  for (int k = 0; k < U; ++k) {
-    const uint32_t Rk = cnt[(int64_t)k * B1 + U];
-    if (k > 0 && Rk != prevR) last = k - 1;
-    pk[k] = last;
-    prevR = Rk;
+// Row classes (ranks with equal R[k] = #{bh <= k}; light-model independent):
+//   pk[k]        largest k' < k with R[k'] < R[k] (else -1): canonical heavy-set twin row
+//   row_start[k] k starts its class;  row_rep[k] class member with the smallest first_pos
+__global__ void __launch_bounds__(1024)
+row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
+                   const int32_t* __restrict__ first_pos, int32_t* pk, int32_t* row_rep,
+                   uint8_t* row_start) {
+  extern __shared__ uint32_t s_R[];
+  for (int k = threadIdx.x; k < U; k += blockDim.x) s_R[k] = cnt[(int64_t)k * B1 + U];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int start = 0;
+  for (int k = 0; k <= U; ++k) {
+    if (k == U || (k > 0 && s_R[k] != s_R[k - 1])) {
+      int best = start;                        // close class [start, k)
+      for (int j = start + 1; j < k; ++j)
+        if (first_pos[j] < first_pos[best]) best = j;
+      for (int j = start; j < k; ++j) {
+        row_rep[j] = best;
+        pk[j] = start - 1;
+        row_start[j] = j == start;
+      }
+      start = k;
+    }
   }
 }
 
@@ -171,9 +244,11 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
     const int64_t c = i - (int64_t)p * cells;
     const int k = (int)(c / g.U), t = (int)(c % g.U);
     const PairConst pc = pcs[p];
-    const CellVal v = eval_cell(g, pc, k, t);
-    const int b = bucket_of(pc, g.nbuckets, v.lat);
-    atomicMin(&bmin[(int64_t)p * g.nbuckets + b], (unsigned long long)order_key(v.fid));
+    if (!class_start(g, slot_cnt(g, pc.slot), k, t)) continue;   // exact duplicate
+    double x, S;
+    cell_numerators(g, pc, k, t, &x, &S);
+    const int b = bucket_of_x(pc, g.nbuckets, x);
+    atomicMin(&bmin[(int64_t)p * g.nbuckets + b], (unsigned long long)order_key(S));
   }
 }
 
@@ -227,20 +302,23 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
   const int64_t total = cells * n_pairs;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
+  const double dn = (double)g.n;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool take = false;
     int p = 0, b = 0, k = 0, t = 0;
-    CellVal v{};
+    double x = 0.0, S = 0.0;
     if (i < total) {
       p = (int)(i / cells);
       const int64_t c = i - (int64_t)p * cells;
       k = (int)(c / g.U);
       t = (int)(c % g.U);
       const PairConst pc = pcs[p];
-      v = eval_cell(g, pc, k, t);
-      b = bucket_of(pc, g.nbuckets, v.lat);
-      take = v.fid <= gpre[(int64_t)p * g.nbuckets + b] + pc.delta2;
+      if (class_start(g, slot_cnt(g, pc.slot), k, t)) {
+        cell_numerators(g, pc, k, t, &x, &S);
+        b = bucket_of_x(pc, g.nbuckets, x);
+        take = S <= gpre[(int64_t)p * g.nbuckets + b] + pc.delta2_S;
+      }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, take);
     if (!mask) continue;
@@ -252,10 +330,10 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
       atomicAdd(&bcnt[(int64_t)p * g.nbuckets + b], 1u);
       if (at < cap) {
         raw.pair[at] = (uint32_t)p;
-        raw.cell[at] = (uint32_t)(k * g.U + t);
+        raw.cell[at] = rep_cell(g, slot_cnt(g, pcs[p].slot), k, t);
         raw.bucket[at] = (uint32_t)b;
-        raw.lat[at] = v.lat;
-        raw.fid[at] = v.fid;
+        raw.lat[at] = __ddiv_rn(x, dn);
+        raw.fid[at] = __ddiv_rn(S, dn);
       }
     }
   }
@@ -263,30 +341,79 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
 
 // ---------------------------------------------- F4: offsets (exclusive scan)
 
-// one block: exclusive scan of n u32 values into u64 offsets (n = pairs * buckets)
-__global__ void __launch_bounds__(kScanThreads)
-exclusive_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
-                      unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long part[kScanThreads];
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t lo = threadIdx.x * per;
-  const int64_t hi = lo + per < n ? lo + per : n;
-  unsigned long long s = 0;
-  for (int64_t i = lo; i < hi; ++i) s += in[i];
-  part[threadIdx.x] = s;
+// Device-wide exclusive scan of n u32 counts into u64 offsets (out[n] = total):
+// tile sums -> one-CTA scan of the tile sums -> per-tile scan with carry-in.
+constexpr int kScanTile = 4096;   // 1024 threads x 4 elements
+
+__device__ __forceinline__ unsigned long long block_exclusive_sum(unsigned long long v,
+                                                                  unsigned long long* total) {
+  __shared__ unsigned long long warp_sums[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
   __syncthreads();
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : 0ull;
-    __syncthreads();
-    part[threadIdx.x] += o;
-    __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned long long ws = lane < nw ? warp_sums[lane] : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, ws, off);
+      if (lane >= off) ws += o;
+    }
+    if (lane < nw) warp_sums[lane] = ws;
   }
-  unsigned long long run = threadIdx.x > 0 ? part[threadIdx.x - 1] : 0ull;
-  for (int64_t i = lo; i < hi; ++i) {
-    out[i] = run;
-    run += in[i];
+  __syncthreads();
+  const unsigned long long before = (warp > 0 ? warp_sums[warp - 1] : 0ull) + incl - v;
+  if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+tile_sum_kernel(const uint32_t* __restrict__ in, int64_t n, unsigned long long* __restrict__ sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
+  unsigned long long v = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v += base + j < n ? in[base + j] : 0u;
+  unsigned long long total;
+  block_exclusive_sum(v, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+tile_offsets_kernel(unsigned long long* __restrict__ sums, int64_t tiles,
+                    unsigned long long* __restrict__ grand_total) {
+  unsigned long long carry = 0;
+  for (int64_t c0 = 0; c0 < tiles; c0 += blockDim.x) {
+    const int64_t i = c0 + threadIdx.x;
+    const unsigned long long v = i < tiles ? sums[i] : 0ull;
+    unsigned long long total;
+    const unsigned long long ex = block_exclusive_sum(v, &total);
+    if (i < tiles) sums[i] = carry + ex;
+    carry += total;
   }
-  if (threadIdx.x == blockDim.x - 1) out[n] = part[blockDim.x - 1];
+  if (threadIdx.x == 0) *grand_total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+tile_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
+                 const unsigned long long* __restrict__ sums, unsigned long long* __restrict__ out) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
+  uint32_t v[4];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) { v[j] = base + j < n ? in[base + j] : 0u; local += v[j]; }
+  unsigned long long run = sums[blockIdx.x] + block_exclusive_sum(local, nullptr);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (base + j < n) out[base + j] = run;
+    run += v[j];
+  }
 }
 
 // ------------------------------------------------------------ F5: scatter
@@ -353,7 +480,7 @@ __global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
                               const unsigned long long* __restrict__ counters_ro, int64_t cap,
                               const unsigned long long* __restrict__ boff,
                               const uint32_t* __restrict__ bcnt, const double* __restrict__ gpre,
-                              const int32_t* __restrict__ pk, Cands grp, uint32_t* kept_bm,
+                              Cands grp, uint32_t* kept_bm,
                               Uncertain un, int64_t ucap, uint32_t* req_bm, uint32_t* req_pair,
                               uint32_t* req_cell, int64_t rcap, unsigned long long* counters) {
   if ((int64_t)counters_ro[0] > cap) return;
@@ -371,17 +498,23 @@ __global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     bool killed = false, unsure = false;
 
     // heavy-set twin with more bypass: equal fidelity, strictly lower latency
-    const int kp = pk[k];
+    const int kp = g.pk[k];
     if (kp >= 0) {
       const uint32_t* C = slot_cnt(g, pc.slot);
       const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
       if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
         const CellVal tw = eval_cell(g, pc, kp, t);
-        if (tw.lat < lat || (tw.lat == lat && grid_index(g, kp, t) < idx)) killed = true;
+        if (tw.lat < lat) {
+          killed = true;
+        } else if (tw.lat == lat) {
+          const uint32_t tc = rep_cell(g, C, kp, t);
+          if (grid_index(g, (int)(tc / g.U), (int)(tc % g.U)) < idx) killed = true;
+        }
       }
     }
     if (!killed) {
-      const double G = gpre[(int64_t)p * g.nbuckets + b];
+      // gpre holds numerators S; fl(S / n) is exactly that cell's fid*
+      const double G = __ddiv_rn(gpre[(int64_t)p * g.nbuckets + b], (double)g.n);
       if (G < fid - pc.delta2) killed = true;
       else if (G <= fid + pc.delta2) unsure = true;
     }
@@ -495,7 +628,7 @@ __global__ void partners_kernel(Grid g, const PairConst* __restrict__ pcs,
     const PairConst pc = pcs[p];
     const CellVal v = eval_cell(g, pc, k, t);
     if (un.universe[e] == 0) {
-      const int b = bucket_of(pc, g.nbuckets, v.lat);
+      const int b = bucket_of(g, pc, k, t);
       const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
       const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
       for (int64_t j = s0 + threadIdx.x; j < s1; j += blockDim.x) {
@@ -626,7 +759,7 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
     if (threadIdx.x == 0) s_kill = have_c ? 0 : 2;
     __syncthreads();
     if (un.universe[e] == 0) {
-      const int b = bucket_of(pc, g.nbuckets, v.lat);
+      const int b = bucket_of(g, pc, k, t);
       const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
       const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
       for (int64_t j = s0 + threadIdx.x; j < s1 && have_c; j += blockDim.x) {
@@ -832,7 +965,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
+  size_t pcs, pk, row_rep, row_start, tsum, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
       counters, pair_rows, pair_off, row_cell, total;
 };
 
@@ -848,6 +981,9 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   const int64_t words = (cells + 31) / 32 * n_pairs;
   L.pcs = take(sizeof(PairConst) * n_pairs);
   L.pk = take(sizeof(int32_t) * U);
+  L.row_rep = take(sizeof(int32_t) * U);
+  L.row_start = take(U);
+  L.tsum = take(8 * (ceil_div(pb, 4096) + 1));
   L.bmin = take(8 * pb);
   L.gpre = take(8 * pb);
   L.bcnt = take(4 * pb);
@@ -870,9 +1006,9 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
 }
 
 static int buckets_for(int U) {
-  int64_t cells = (int64_t)U * U;
+  const int64_t cells = (int64_t)U * U;
   int64_t b = 1024;
-  while (b < cells / 8 && b < (1 << 17)) b <<= 1;
+  while (b < cells / 4 && b < (1 << 18)) b <<= 1;
   return (int)b;
 }
 
@@ -913,6 +1049,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
 
   PairConst* pcs = (PairConst*)P(L.pcs);
   int32_t* pk = (int32_t*)P(L.pk);
+  int32_t* row_rep = (int32_t*)P(L.row_rep);
+  uint8_t* row_start = (uint8_t*)P(L.row_start);
+  unsigned long long* tsum = (unsigned long long*)P(L.tsum);
   unsigned long long* bmin = (unsigned long long*)P(L.bmin);
   double* gpre = (double*)P(L.gpre);
   uint32_t* bcnt = (uint32_t*)P(L.bcnt);
@@ -944,10 +1083,11 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * 8, st));
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
-         n_thresholds, first_pos, words_per_pair * 32};
+         n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start};
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
-  twin_row_kernel<<<1, 1, 0, st>>>(pre_cnt + (int64_t)0, n_unique, n_unique + 1, pk);
+  row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
+                                                            first_pos, pk, row_rep, row_start);
   HADIS_LAUNCH_CHECK();
 
   const int64_t total_cells = cells * n_pairs;
@@ -957,10 +1097,15 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   bucket_prefix_kernel<<<n_pairs, kScanThreads, 0, st>>>(bmin, nb, gpre);
   filter_kernel<<<(unsigned)grid_cells, kCellThreads, 0, st>>>(g, pcs, n_pairs, gpre, bcnt, raw,
                                                               cand_cap, counters);
-  exclusive_scan_kernel<<<1, kScanThreads, 0, st>>>(bcnt, pb, boff);
+  {
+    const int64_t tiles = ceil_div(pb, kScanTile);
+    tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum);
+    tile_offsets_kernel<<<1, kScanThreads, 0, st>>>(tsum, tiles, boff + pb);
+    tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
+  }
   scatter_kernel<<<kNumSMs * 4, 256, 0, st>>>(raw, counters, cand_cap, nb, boff, bcur, grp);
   HADIS_LAUNCH_CHECK();
-  decide_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre, pk,
+  decide_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, kept, un, exact_cap, reqbm, req_pair, req_cell,
                                              exact_cap, counters);
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
@@ -995,6 +1140,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   finish_stats_kernel<<<1, 1, 0, st>>>(counters, cand_cap, exact_cap, exact_cap, stats);
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(20);
   return HADIS_OK;
 }
 
@@ -1010,5 +1156,6 @@ extern "C" int hadis_fid_exact(const double* h, const double* scores, int64_t n,
   fid_exact_kernel<<<grid, kPwThreads, 0, (cudaStream_t)stream>>>(
       h, scores, n, n_cells, cell_slot, cell_theta, cell_tau, cell_params, out_fid);
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(1);
   return HADIS_OK;
 }

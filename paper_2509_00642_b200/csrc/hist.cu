@@ -187,6 +187,7 @@ extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, 
         (unsigned long long*)hist_hsum, bad_records);
   }
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(1);
   return HADIS_OK;
 }
 
@@ -203,5 +204,6 @@ extern "C" int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t 
   scan_cols_kernel<<<(unsigned)ceil_div(cols, 128), 128, 0, st>>>(
       hist_cnt, (unsigned long long*)hist_hsum, n_light, B1);
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(2);
   return HADIS_OK;
 }

@@ -308,5 +308,6 @@ extern "C" int hadis_solve_many(int32_t n_rows, const int32_t* row_model, const 
   reduce_points_kernel<<<n_points, kPlanThreads, 0, st>>>(in, 1, nblk, partial, need_fb, plan_row,
                                                           plan_x, plan_b, plan_path, plan_flags);
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(4);
   return HADIS_OK;
 }

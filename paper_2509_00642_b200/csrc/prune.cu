@@ -170,10 +170,12 @@ extern "C" int hadis_pareto_prune(const double* lat, const double* qual, int64_t
     if (in0) merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a0, b0, i0, n, run, a1, b1, i1);
     else merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a1, b1, i1, n, run, a0, b0, i0);
     HADIS_LAUNCH_CHECK();
+    hadis_count_launches(1);
     in0 = !in0;
   }
   keep_compact_kernel<<<1, kPruneThreads, 0, st>>>(in0 ? b0 : b1, in0 ? i0 : i1, n, out_idx,
                                                    out_count);
   HADIS_LAUNCH_CHECK();
+  hadis_count_launches(2);
   return HADIS_OK;
 }

@@ -227,12 +227,42 @@ class DeviceTable:
     stats: dict
 
 
+class ProfilePlan:
+    """Device-resident description of one (threshold grid, pair set) job:
+    sorted distinct thresholds, first positions, pair slots/parameters and the
+    output/workspace capacities learned from previous runs."""
+
+    def __init__(self, prof, thresholds, pairs):
+        torch = prof.torch
+        dev = prof.device
+        self.grid = GridSpec.build(thresholds)
+        self.pairs = pair_list(prof.pool) if pairs is None else list(pairs)
+        if not self.pairs:
+            raise ProfileError("profile_records: no pairs to profile")
+        slots = sorted({i for i, _ in self.pairs})
+        self.slot0 = slots[0]
+        self.n_light = slots[-1] - slots[0] + 1
+        self.U = len(self.grid.unique)
+        self.P = len(self.pairs)
+        self.d_u = torch.tensor(self.grid.unique, dtype=torch.float64, device=dev)
+        self.d_first = torch.tensor(self.grid.first_pos, dtype=torch.int32, device=dev)
+        self.d_slot = torch.tensor([i - self.slot0 for i, _ in self.pairs], dtype=torch.int32,
+                                   device=dev)
+        self.d_params = torch.from_numpy(pair_params(prof.pool, self.pairs)).to(dev)
+        cells = self.U * self.U * self.P
+        cand = int(min(cells, max(1 << 20, cells // 8)))
+        self.caps = (cand, 2048, int(min(cells, cand + self.U * self.P)))
+        self.cells = cells
+
+
 class GridProfiler:
     """Records resident in HBM + the K1..K4 device pipeline.
 
     ``h`` is float64[N] and ``scores`` float64[L, N] (row i = pool model i as
     the light stage), both in ``stable_text_key`` order and already on the
-    device (torch tensors) or host arrays copied once at construction."""
+    device (torch tensors) or host arrays copied once at construction.
+    ``run`` profiles one threshold grid; ``launch``/``finish`` split it into an
+    asynchronous enqueue and a synchronising check for pipelined callers."""
 
     def __init__(self, pool, h, scores, device=None):
         torch = _lib.torch_cuda()
@@ -252,64 +282,51 @@ class GridProfiler:
         self.lib = _lib.load()
         self.shift = self.lib.hadis_hfix_shift(self.n)
         self._ws = None
-        self._caps = None
+        self._plans = {}
 
-    # -- K1 + K2 ---------------------------------------------------------
-    def histograms(self, grid: GridSpec, slot0: int, n_light: int, stream=None):
+    def plan(self, thresholds=THRESHOLD_GRID, pairs=None) -> ProfilePlan:
+        key = (tuple(float(t) for t in thresholds), None if pairs is None else tuple(pairs))
+        pl = self._plans.get(key)
+        if pl is None:
+            pl = self._plans[key] = ProfilePlan(self, thresholds, pairs)
+        return pl
+
+    def run(self, thresholds=THRESHOLD_GRID, pairs=None, exact_fid=False, stream=None):
+        """Profile ``pairs`` (default: every light<heavy pair); returns a DeviceTable."""
+        return self.finish(self.launch(self.plan(thresholds, pairs), exact_fid, stream))
+
+    def launch(self, plan: ProfilePlan, exact_fid=False, stream=None, events=None):
+        """Enqueue K1 (bin + histogram), K2 (2-D scan) and K3/K4 (frontier) on
+        ``stream``; no host synchronisation.  ``events`` (optional list of 4
+        torch.cuda.Event) brackets K1 | K2 | K3+K4 for per-kernel timing."""
         torch = self.torch
-        U = len(grid.unique)
-        bins = (U + 1) * (U + 1) * n_light
-        cnt = torch.empty(bins, dtype=torch.int32, device=self.device)
-        hsum = torch.empty(bins, dtype=torch.int64, device=self.device)
-        bad = torch.empty(1, dtype=torch.int32, device=self.device)
-        d_u = torch.tensor(grid.unique, dtype=torch.float64, device=self.device)
+        dev = self.device
         st = _lib.stream_handle(stream)
-        scores = self.scores[slot0:slot0 + n_light]
-        _lib.check(self.lib.hadis_bin_hist(_lib.ptr(self.h), _lib.ptr(scores), self.n, n_light,
-                                           _lib.ptr(d_u), U, self.shift, _lib.ptr(cnt),
-                                           _lib.ptr(hsum), _lib.ptr(bad), st), "hadis_bin_hist")
-        _lib.check(self.lib.hadis_hist_scan(_lib.ptr(cnt), _lib.ptr(hsum), n_light, U, st),
-                   "hadis_hist_scan")
-        return cnt, hsum, bad, d_u
+        bins = (plan.U + 1) * (plan.U + 1) * plan.n_light
+        state = dict(plan=plan, exact_fid=exact_fid, stream=stream,
+                     cnt=torch.empty(bins, dtype=torch.int32, device=dev),
+                     hsum=torch.empty(bins, dtype=torch.int64, device=dev),
+                     bad=torch.empty(1, dtype=torch.int32, device=dev),
+                     scores=self.scores[plan.slot0:plan.slot0 + plan.n_light])
+        p = _lib.ptr
+        rec = (lambda i: events[i].record(stream)) if events is not None else (lambda i: None)
+        rec(0)
+        _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
+                                           p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
+                                           p(state["hsum"]), p(state["bad"]), st), "hadis_bin_hist")
+        rec(1)
+        _lib.check(self.lib.hadis_hist_scan(p(state["cnt"]), p(state["hsum"]), plan.n_light,
+                                            plan.U, st), "hadis_hist_scan")
+        rec(2)
+        self._frontier(state, plan.caps)
+        rec(3)
+        return state
 
-    # -- K3 + K4 ---------------------------------------------------------
-    def run(self, thresholds=THRESHOLD_GRID, pairs=None, exact_fid=False, stream=None,
-            caps=None, sync=True):
-        """Profile ``pairs`` (default: all light<heavy pairs).  Returns a DeviceTable.
-
-        With ``sync=False`` nothing waits for the device: the caller must call
-        ``finish(...)`` (which synchronises) before reading results."""
+    def _frontier(self, state, caps):
         torch = self.torch
-        grid = GridSpec.build(thresholds)
-        pairs = pair_list(self.pool) if pairs is None else list(pairs)
-        if not pairs:
-            raise ProfileError("profile_records: no pairs to profile")
-        U = len(grid.unique)
-        slots = sorted({i for i, _ in pairs})
-        slot0, n_light = slots[0], slots[-1] - slots[0] + 1
-        cnt, hsum, bad, d_u = self.histograms(grid, slot0, n_light, stream)
-        d_slot = torch.tensor([i - slot0 for i, _ in pairs], dtype=torch.int32, device=self.device)
-        d_params = torch.from_numpy(pair_params(self.pool, pairs)).to(self.device)
-        d_first = torch.tensor(grid.first_pos, dtype=torch.int32, device=self.device)
-        scores = self.scores[slot0:slot0 + n_light]
-        P = len(pairs)
-        if caps is None:
-            cells = U * U * P
-            cand = int(min(cells, max(1 << 20, cells // 8)))
-            caps = (cand, 2048, int(min(cells, cand + U * P)))
-        state = dict(grid=grid, pairs=pairs, cnt=cnt, hsum=hsum, bad=bad, d_u=d_u, d_slot=d_slot,
-                     d_params=d_params, d_first=d_first, scores=scores, exact_fid=exact_fid,
-                     stream=stream)
-        self._launch(state, caps)
-        if not sync:
-            return state
-        return self.finish(state)
-
-    def _launch(self, state, caps):
-        torch = self.torch
+        plan = state["plan"]
         cand_cap, exact_cap, out_cap = caps
-        grid, pairs = state["grid"], state["pairs"]
-        U, P = len(grid.unique), len(pairs)
+        U, P = plan.U, plan.P
         ws_bytes = self.lib.hadis_frontier_workspace_bytes(P, U, cand_cap, exact_cap, out_cap)
         if ws_bytes == 0:
             raise ProfileError("profile_records: invalid frontier sizes")
@@ -326,8 +343,8 @@ class GridProfiler:
         stats = torch.zeros(_lib.ST_PAIR0 + P, dtype=torch.int64, device=dev)
         p = _lib.ptr
         _lib.check(self.lib.hadis_pair_frontiers(
-            p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(state["d_slot"]),
-            p(state["d_params"]), p(state["d_first"]), len(grid.thresholds), p(state["d_u"]),
+            p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(plan.d_slot),
+            p(plan.d_params), p(plan.d_first), len(plan.grid.thresholds), p(plan.d_u),
             p(self.h), p(state["scores"]), 1 if state["exact_fid"] else 0, p(self._ws), ws_bytes,
             cand_cap, exact_cap, out_cap, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]),
             p(out["r_light"]), p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
@@ -336,28 +353,29 @@ class GridProfiler:
 
     def finish(self, state) -> DeviceTable:
         """Synchronise, check device-side status, grow capacities and rerun if needed."""
+        plan = state["plan"]
         for _ in range(6):
             stats = state["stats"].cpu().tolist()
             if int(state["bad"].item()):
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW] == 0:
                 break
-            cand_cap, exact_cap, out_cap = state["caps"]
-            U, P = len(state["grid"].unique), len(state["pairs"])
-            cells = U * U * P
-            cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
-            out_cap = int(min(cells, max(out_cap * 2, cand_cap + U * P)))
             if stats[_lib.ST_OVERFLOW] & (2 | 4 | 64):
                 raise ProfileError("profile_records: too many exactness-critical cells "
                                    f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
-            self._launch(state, (cand_cap, exact_cap, out_cap))
+            cand_cap, exact_cap, out_cap = state["caps"]
+            cells = plan.cells
+            cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
+            out_cap = int(min(cells, max(out_cap * 2, cand_cap + plan.U * plan.P)))
+            plan.caps = (cand_cap, exact_cap, out_cap)
+            self._frontier(state, plan.caps)
         else:
             raise ProfileError("profile_records: capacity retries exhausted")
         n_rows = stats[_lib.ST_ROWS]
         out = state["out"]
         return DeviceTable(
-            pairs=state["pairs"], n_rows=n_rows,
-            pair_rows=stats[_lib.ST_PAIR0:_lib.ST_PAIR0 + len(state["pairs"])],
+            pairs=plan.pairs, n_rows=n_rows,
+            pair_rows=stats[_lib.ST_PAIR0:_lib.ST_PAIR0 + plan.P],
             pair=out["pair"][:n_rows], theta_pos=out["theta_pos"][:n_rows],
             tau_pos=out["tau_pos"][:n_rows], r_light=out["r_light"][:n_rows],
             r_heavy=out["r_heavy"][:n_rows], fid=out["fid"][:n_rows], lat=out["lat"][:n_rows],
