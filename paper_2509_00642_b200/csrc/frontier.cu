@@ -56,6 +56,7 @@ struct Grid {
   const int32_t* pk;        // twin row: largest k' < k with R[k'] < R[k], else -1
   const int32_t* row_rep;   // rank with the smallest first_pos in k's row class
   const uint8_t* row_start; // 1 if k starts its row class (R[k-1] < R[k])
+  const int32_t* sorted;    // *sorted != 0: first_pos increases with rank (sorted list)
 };
 
 struct CellVal {
@@ -138,12 +139,14 @@ __device__ __forceinline__ bool class_start(const Grid& g, const uint32_t* C, in
 }
 
 // Rank with the smallest first position in the tau-run of row k containing t.
-__device__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t) {
+__device__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t, bool run_start = false) {
+  if (run_start && *g.sorted) return t;       // smallest rank == smallest position
   const uint32_t* row = C + (int64_t)k * g.B1;
   const uint32_t v = row[t];
   int lo = 0, hi = t;                         // first index with row[idx] == v
   while (lo < hi) { const int mid = (lo + hi) >> 1; if (row[mid] < v) lo = mid + 1; else hi = mid; }
   const int start = lo;
+  if (*g.sorted) return start;
   lo = t + 1; hi = g.U;                       // first index with row[idx] > v
   while (lo < hi) { const int mid = (lo + hi) >> 1; if (row[mid] <= v) lo = mid + 1; else hi = mid; }
   int best = start;
@@ -153,8 +156,9 @@ __device__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t) {
 }
 
 // representative (smallest grid index) cell of (k, t)'s duplicate class
-__device__ __forceinline__ uint32_t rep_cell(const Grid& g, const uint32_t* C, int k, int t) {
-  return (uint32_t)(g.row_rep[k] * g.U + rep_tau(g, C, k, t));
+__device__ __forceinline__ uint32_t rep_cell(const Grid& g, const uint32_t* C, int k, int t,
+                                             bool run_start = false) {
+  return (uint32_t)(g.row_rep[k] * g.U + rep_tau(g, C, k, t, run_start));
 }
 
 __device__ __forceinline__ int64_t grid_index(const Grid& g, int k, int t) {
@@ -208,11 +212,18 @@ __global__ void pair_const_kernel(int n_pairs, const int32_t* __restrict__ pair_
 __global__ void __launch_bounds__(1024)
 row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
                    const int32_t* __restrict__ first_pos, int32_t* pk, int32_t* row_rep,
-                   uint8_t* row_start) {
+                   uint8_t* row_start, int32_t* sorted) {
   extern __shared__ uint32_t s_R[];
-  for (int k = threadIdx.x; k < U; k += blockDim.x) s_R[k] = cnt[(int64_t)k * B1 + U];
+  __shared__ int s_unsorted;
+  if (threadIdx.x == 0) s_unsorted = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < U; k += blockDim.x) {
+    s_R[k] = cnt[(int64_t)k * B1 + U];
+    if (k > 0 && first_pos[k] < first_pos[k - 1]) s_unsorted = 1;
+  }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  *sorted = !s_unsorted;
   int start = 0;
   for (int k = 0; k <= U; ++k) {
     if (k == U || (k > 0 && s_R[k] != s_R[k - 1])) {
@@ -256,31 +267,59 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
 
 constexpr int kScanThreads = 1024;
 
+__device__ __forceinline__ unsigned long long block_exclusive_min(unsigned long long v,
+                                                                  unsigned long long* total) {
+  __shared__ unsigned long long warp_min[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl = min(incl, o);
+  }
+  unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = ~0ull;
+  if (lane == 31) warp_min[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned long long w = lane < nw ? warp_min[lane] : ~0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w = min(w, o);
+    }
+    if (lane < nw) warp_min[lane] = w;
+  }
+  __syncthreads();
+  const unsigned long long before = warp > 0 ? min(warp_min[warp - 1], excl) : excl;
+  *total = warp_min[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+// per pair: exclusive prefix-min over bucket minima, tiles of 4 x blockDim keys
 __global__ void __launch_bounds__(kScanThreads)
 bucket_prefix_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
                      double* __restrict__ gpre) {
-  __shared__ unsigned long long part[kScanThreads];
   const int p = blockIdx.x;
   const unsigned long long* src = bmin + (int64_t)p * nbuckets;
   double* dst = gpre + (int64_t)p * nbuckets;
-  const int per = (nbuckets + blockDim.x - 1) / blockDim.x;
-  const int lo = threadIdx.x * per;
-  const int hi = min(nbuckets, lo + per);
-  unsigned long long m = ~0ull;
-  for (int i = lo; i < hi; ++i) m = min(m, src[i]);
-  part[threadIdx.x] = m;
-  __syncthreads();
-  // Hillis-Steele inclusive min-scan over the per-thread minima
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : ~0ull;
-    __syncthreads();
-    part[threadIdx.x] = min(part[threadIdx.x], o);
-    __syncthreads();
-  }
-  unsigned long long run = threadIdx.x > 0 ? part[threadIdx.x - 1] : ~0ull;
-  for (int i = lo; i < hi; ++i) {
-    dst[i] = run == ~0ull ? INFINITY : from_order_key(run);
-    run = min(run, src[i]);
+  unsigned long long carry = ~0ull;
+  for (int base = 0; base < nbuckets; base += 4 * blockDim.x) {
+    const int i0 = base + 4 * threadIdx.x;
+    unsigned long long v[4];
+    unsigned long long m = ~0ull;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { v[j] = i0 + j < nbuckets ? src[i0 + j] : ~0ull; m = min(m, v[j]); }
+    unsigned long long total;
+    unsigned long long run = min(carry, block_exclusive_min(m, &total));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j < nbuckets) dst[i0 + j] = run == ~0ull ? INFINITY : from_order_key(run);
+      run = min(run, v[j]);
+    }
+    carry = min(carry, total);
   }
 }
 
@@ -330,7 +369,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
       atomicAdd(&bcnt[(int64_t)p * g.nbuckets + b], 1u);
       if (at < cap) {
         raw.pair[at] = (uint32_t)p;
-        raw.cell[at] = rep_cell(g, slot_cnt(g, pcs[p].slot), k, t);
+        raw.cell[at] = rep_cell(g, slot_cnt(g, pcs[p].slot), k, t, true);
         raw.bucket[at] = (uint32_t)b;
         raw.lat[at] = __ddiv_rn(x, dn);
         raw.fid[at] = __ddiv_rn(S, dn);
@@ -803,39 +842,49 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
 
 // ------------------------------------------------------------- F12: emit
 
+// The kept bitmap is cut into chunks of kEmitWords words (per pair); chunk
+// popcounts -> device-wide scan -> one CTA per chunk writes its rows, so rows
+// come out pair-major and, within a pair, in (theta rank, tau rank) order.
+constexpr int kEmitWords = 256;   // = emit CTA size
+
 __global__ void __launch_bounds__(kScanThreads)
-count_rows_kernel(const uint32_t* __restrict__ kept_bm, int64_t words_per_pair,
-                  unsigned long long* __restrict__ pair_rows) {
-  __shared__ unsigned long long part[kScanThreads];
-  const int p = blockIdx.x;
-  const uint32_t* w = kept_bm + (int64_t)p * words_per_pair;
-  unsigned long long s = 0;
-  for (int64_t i = threadIdx.x; i < words_per_pair; i += blockDim.x) s += __popc(w[i]);
-  part[threadIdx.x] = s;
+count_chunks_kernel(const uint32_t* __restrict__ kept_bm, int64_t words_per_pair, int n_chunks,
+                    uint32_t* __restrict__ chunk_rows) {
+  const int p = blockIdx.y, c = blockIdx.x;
+  const int64_t wi = (int64_t)c * kEmitWords + threadIdx.x;
+  uint32_t v = wi < words_per_pair ? __popc(kept_bm[(int64_t)p * words_per_pair + wi]) : 0u;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __shared__ uint32_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
   __syncthreads();
-  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-    if (threadIdx.x < off) part[threadIdx.x] += part[threadIdx.x + off];
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t t = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (threadIdx.x == 0) chunk_rows[(int64_t)p * n_chunks + c] = t;
   }
-  if (threadIdx.x == 0) pair_rows[p] = part[0];
 }
 
-__global__ void pair_offsets_kernel(const unsigned long long* __restrict__ pair_rows, int n_pairs,
-                                    unsigned long long* __restrict__ pair_off, int64_t* stats,
-                                    int64_t out_cap, unsigned long long* counters) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  unsigned long long run = 0;
-  for (int p = 0; p < n_pairs; ++p) {
-    pair_off[p] = run;
-    stats[HADIS_ST_PAIR0 + p] = (int64_t)pair_rows[p];
-    run += pair_rows[p];
+__global__ void pair_offsets_kernel(const unsigned long long* __restrict__ chunk_off, int n_chunks,
+                                    int n_pairs, unsigned long long* __restrict__ pair_off,
+                                    int64_t* stats, int64_t out_cap, unsigned long long* counters) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n_pairs) {
+    const unsigned long long a = chunk_off[(int64_t)p * n_chunks];
+    const unsigned long long b = chunk_off[(int64_t)(p + 1) * n_chunks];
+    pair_off[p] = a;
+    stats[HADIS_ST_PAIR0 + p] = (int64_t)(b - a);
   }
-  pair_off[n_pairs] = run;
-  stats[HADIS_ST_ROWS] = (int64_t)run;
-  stats[HADIS_ST_CANDIDATES] = (int64_t)counters[0];
-  stats[HADIS_ST_UNCERTAIN] = (int64_t)counters[1];
-  stats[HADIS_ST_EXACT_CELLS] = (int64_t)counters[2];
-  if ((int64_t)run > out_cap) counters[4] |= 8ull;
+  if (p == 0) {
+    const unsigned long long run = chunk_off[(int64_t)n_pairs * n_chunks];
+    pair_off[n_pairs] = run;
+    stats[HADIS_ST_ROWS] = (int64_t)run;
+    stats[HADIS_ST_CANDIDATES] = (int64_t)counters[0];
+    stats[HADIS_ST_UNCERTAIN] = (int64_t)counters[1];
+    stats[HADIS_ST_EXACT_CELLS] = (int64_t)counters[2];
+    if ((int64_t)run > out_cap) counters[4] |= 8ull;
+  }
 }
 
 struct Rows {
@@ -849,51 +898,42 @@ struct Rows {
   uint32_t* cell;   // workspace: k * U + t, for exact patches
 };
 
-__global__ void __launch_bounds__(kScanThreads)
+// bits -> cell list in shared memory -> one row per thread (coalesced stores)
+__global__ void __launch_bounds__(kEmitWords)
 emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __restrict__ kept_bm,
-                 int64_t words_per_pair, const unsigned long long* __restrict__ pair_off,
-                 int64_t out_cap, Rows out) {
-  __shared__ unsigned long long part[kScanThreads];
-  const int p = blockIdx.x;
-  const PairConst pc = pcs[p];
-  const uint32_t* w = kept_bm + (int64_t)p * words_per_pair;
+                 int64_t words_per_pair, int n_chunks,
+                 const unsigned long long* __restrict__ chunk_off, int64_t out_cap, Rows out) {
+  __shared__ uint32_t s_cell[kEmitWords * 32];
+  const int p = blockIdx.y, ch = blockIdx.x;
+  const int64_t wi = (int64_t)ch * kEmitWords + threadIdx.x;
+  const uint32_t word = wi < words_per_pair ? kept_bm[(int64_t)p * words_per_pair + wi] : 0u;
   const int64_t cells = (int64_t)g.U * g.U;
-  unsigned long long base = pair_off[p];
+  unsigned long long total;
+  int at = (int)block_exclusive_sum((unsigned long long)__popc(word), &total);
+  uint32_t bits = word;
+  while (bits) {
+    const int b = __ffs(bits) - 1;
+    bits &= bits - 1;
+    s_cell[at++] = (uint32_t)(wi * 32 + b);
+  }
+  __syncthreads();
+  const PairConst pc = pcs[p];
   const double dn = (double)g.n;
-  for (int64_t w0 = 0; w0 < words_per_pair; w0 += blockDim.x) {
-    const int64_t wi = w0 + threadIdx.x;
-    const uint32_t word = wi < words_per_pair ? w[wi] : 0u;
-    part[threadIdx.x] = __popc(word);
-    __syncthreads();
-    for (int off = 1; off < blockDim.x; off <<= 1) {
-      unsigned long long o = threadIdx.x >= off ? part[threadIdx.x - off] : 0ull;
-      __syncthreads();
-      part[threadIdx.x] += o;
-      __syncthreads();
-    }
-    unsigned long long at = base + part[threadIdx.x] - __popc(word);
-    uint32_t bits = word;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const int64_t c = wi * 32 + b;
-      if (c < cells && (int64_t)at < out_cap) {
-        const int k = (int)(c / g.U), t = (int)(c % g.U);
-        const CellVal v = eval_cell(g, pc, k, t);
-        out.pair[at] = p;
-        out.theta_pos[at] = g.first_pos[k];
-        out.tau_pos[at] = g.first_pos[t];
-        out.r_light[at] = __ddiv_rn((double)v.n_keep_light, dn);
-        out.r_heavy[at] = __ddiv_rn((double)v.n_heavy, dn);
-        out.fid[at] = v.fid;
-        out.lat[at] = v.lat;
-        out.cell[at] = (uint32_t)c;
-      }
-      ++at;
-    }
-    const unsigned long long tot = part[blockDim.x - 1];
-    __syncthreads();
-    base += tot;
+  const unsigned long long base = chunk_off[(int64_t)p * n_chunks + ch];
+  for (int i = threadIdx.x; i < (int)total; i += blockDim.x) {
+    const int64_t c = s_cell[i];
+    const int64_t r = (int64_t)base + i;
+    if (c >= cells || r >= out_cap) continue;
+    const int k = (int)(c / g.U), t = (int)(c % g.U);
+    const CellVal v = eval_cell(g, pc, k, t);
+    out.pair[r] = p;
+    out.theta_pos[r] = g.first_pos[k];
+    out.tau_pos[r] = g.first_pos[t];
+    out.r_light[r] = __ddiv_rn((double)v.n_keep_light, dn);
+    out.r_heavy[r] = __ddiv_rn((double)v.n_heavy, dn);
+    out.fid[r] = v.fid;
+    out.lat[r] = v.lat;
+    out.cell[r] = (uint32_t)c;
   }
 }
 
@@ -965,8 +1005,8 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, tsum, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
-      counters, pair_rows, pair_off, row_cell, total;
+  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
+      counters, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -983,6 +1023,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.pk = take(sizeof(int32_t) * U);
   L.row_rep = take(sizeof(int32_t) * U);
   L.row_start = take(U);
+  L.sorted = take(4);
   L.tsum = take(8 * (ceil_div(pb, 4096) + 1));
   L.bmin = take(8 * pb);
   L.gpre = take(8 * pb);
@@ -998,7 +1039,10 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
   L.req[0] = take(4 * ecap); L.req[1] = take(4 * ecap); L.req[2] = take(8 * ecap);
   L.counters = take(8 * 8);
-  L.pair_rows = take(8 * n_pairs);
+  const int64_t n_cw = ceil_div((cells + 31) / 32, 256) * n_pairs;    // emit chunks
+  L.pair_rows = take(4 * n_cw);
+  L.chunk_off = take(8 * (n_cw + 1));
+  L.ctsum = take(8 * (ceil_div(n_cw, 4096) + 1));
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
   L.total = at;
@@ -1051,6 +1095,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   int32_t* pk = (int32_t*)P(L.pk);
   int32_t* row_rep = (int32_t*)P(L.row_rep);
   uint8_t* row_start = (uint8_t*)P(L.row_start);
+  int32_t* sorted = (int32_t*)P(L.sorted);
   unsigned long long* tsum = (unsigned long long*)P(L.tsum);
   unsigned long long* bmin = (unsigned long long*)P(L.bmin);
   double* gpre = (double*)P(L.gpre);
@@ -1068,7 +1113,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* req_cell = (uint32_t*)P(L.req[1]);
   double* req_fid = (double*)P(L.req[2]);
   unsigned long long* counters = (unsigned long long*)P(L.counters);
-  unsigned long long* pair_rows = (unsigned long long*)P(L.pair_rows);
+  uint32_t* chunk_rows = (uint32_t*)P(L.pair_rows);
+  unsigned long long* chunk_off = (unsigned long long*)P(L.chunk_off);
+  unsigned long long* ctsum = (unsigned long long*)P(L.ctsum);
   unsigned long long* pair_off = (unsigned long long*)P(L.pair_off);
   uint32_t* row_cell = (uint32_t*)P(L.row_cell);
 
@@ -1083,11 +1130,12 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * 8, st));
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
-         n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start};
+         n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
-                                                            first_pos, pk, row_rep, row_start);
+                                                            first_pos, pk, row_rep, row_start,
+                                                            sorted);
   HADIS_LAUNCH_CHECK();
 
   const int64_t total_cells = cells * n_pairs;
@@ -1125,12 +1173,22 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   resolve_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, exact_cap, un,
                                           grp, boff, req_pair, req_cell, req_fid, kept, counters);
   HADIS_LAUNCH_CHECK();
-  count_rows_kernel<<<n_pairs, kScanThreads, 0, st>>>(kept, words_per_pair, pair_rows);
-  pair_offsets_kernel<<<1, 1, 0, st>>>(pair_rows, n_pairs, pair_off, stats, out_cap, counters);
+  const int n_chunks = (int)ceil_div(words_per_pair, kEmitWords);
+  const int64_t n_cw = (int64_t)n_chunks * n_pairs;
+  count_chunks_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(kept, words_per_pair,
+                                                                        n_chunks, chunk_rows);
+  {
+    const int64_t tiles = ceil_div(n_cw, kScanTile);
+    tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(chunk_rows, n_cw, ctsum);
+    tile_offsets_kernel<<<1, kScanThreads, 0, st>>>(ctsum, tiles, chunk_off + n_cw);
+    tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(chunk_rows, n_cw, ctsum, chunk_off);
+  }
+  pair_offsets_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
+      chunk_off, n_chunks, n_pairs, pair_off, stats, out_cap, counters);
   Rows out{out_pair, out_theta_pos, out_tau_pos, out_r_light, out_r_heavy, out_fid, out_lat,
            row_cell};
-  emit_rows_kernel<<<n_pairs, kScanThreads, 0, st>>>(g, pcs, kept, words_per_pair, pair_off,
-                                                     out_cap, out);
+  emit_rows_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(
+      g, pcs, kept, words_per_pair, n_chunks, chunk_off, out_cap, out);
   if (exact_fid) {
     exact_rows_kernel<<<kNumSMs * 2, kPwThreads, 0, st>>>(g, pcs, thr_unique, h, scores,
                                                           pair_off, n_pairs, out_cap, out);
@@ -1140,7 +1198,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   finish_stats_kernel<<<1, 1, 0, st>>>(counters, cand_cap, exact_cap, exact_cap, stats);
   HADIS_LAUNCH_CHECK();
-  hadis_count_launches(20);
+  hadis_count_launches(24);
   return HADIS_OK;
 }
 

@@ -130,7 +130,21 @@ __global__ void scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long*
   unsigned long long* s = hs + l * B1 * B1 + t;
   uint32_t acc_c = 0;
   unsigned long long acc_s = 0;
-  for (int k = 0; k < B1; ++k) {
+  int k = 0;
+  for (; k + 8 <= B1; k += 8) {       // 8 independent loads in flight per thread
+    uint32_t vc[8];
+    unsigned long long vs[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vs[j] = s[(int64_t)(k + j) * B1]; }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      acc_c += vc[j];
+      acc_s += vs[j];
+      c[(int64_t)(k + j) * B1] = acc_c;
+      s[(int64_t)(k + j) * B1] = acc_s;
+    }
+  }
+  for (; k < B1; ++k) {
     acc_c += c[(int64_t)k * B1];
     acc_s += s[(int64_t)k * B1];
     c[(int64_t)k * B1] = acc_c;
