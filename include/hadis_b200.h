@@ -56,8 +56,29 @@ int64_t hadis_kernel_launches(void);
 /* ------------------------------------------------------------------------- */
 
 /* Fixed-point scale for hardness sums: h_fix = floor(h * 2^shift), with
- * shift = 63 - bit_length(n) so that every sum of n values fits in 63 bits. */
+ * shift = min(48, 63 - bit_length(n)) so every sum of n values fits in 63 bits
+ * and one record's h_fix splits into three 16-bit K1 shared-memory limbs. */
 int hadis_hfix_shift(int64_t n);
+
+/* Record-store ingest: order records by hardness (ties by original index) and
+ * gather the n_rows score rows (row stride n) into the same order.  perm (may
+ * be NULL) receives the original index of each sorted position; bad_records
+ * counts hardness values that are NaN or outside [0, 1]. */
+size_t hadis_records_workspace_bytes(int64_t n);
+int hadis_records_sort(const double* h, const double* scores, int64_t n, int32_t n_rows,
+                       double* h_sorted, double* scores_sorted, uint32_t* perm,
+                       uint32_t* bad_records, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* K1 on a hardness-sorted record store (profiler.py:138, 145-150): same
+ * histogram as hadis_bin_hist, built without global atomics -- each row of
+ * equal bh is a contiguous run of sorted records, so one CTA per (row chunk,
+ * light model) accumulates in shared memory and stores the row. */
+size_t hadis_bin_hist_sorted_workspace_bytes(int32_t n_unique);
+int hadis_bin_hist_sorted(const double* h_sorted, const double* scores_sorted, int64_t n,
+                          int32_t n_light, const double* thr_unique, int32_t n_unique,
+                          int32_t hfix_shift, uint32_t* hist_cnt, uint64_t* hist_hsum,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* K1 -- bin + 2-D histogram (profiler.py:138, 145-150: bypass h > theta,
  * reject score < tau).  For every record q and light model l:

@@ -73,4 +73,9 @@ __device__ __forceinline__ int count_less_equal(const double* u, int n, double x
   return lo;
 }
 
+// prune.cu: ascending sort of (k1, k2, index) keys (k2 may be null)
+size_t sort_workspace_bytes(int64_t n);
+int sort_keys(const double* k1, const double* k2, int64_t n, void* workspace, cudaStream_t st,
+              const uint32_t** sorted_idx, const unsigned long long** sorted_k2);
+
 }  // namespace hadis

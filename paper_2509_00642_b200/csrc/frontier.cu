@@ -25,6 +25,7 @@
 //   F8-F11             partners of uncertain cells -> numpy-exact fid -> decide
 //   F12 emit           kept-cell bitmap -> rows in (theta, tau) order
 //   F13/F14            exact fidelity patch for emitted rows
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -691,6 +692,56 @@ __global__ void partners_kernel(Grid g, const PairConst* __restrict__ pcs,
 
 // ------------------------------------------------ F9: numpy-exact fidelities
 
+// Cells to emulate are (pair, cell) lists of length *count (capped by cap).
+struct CellList {
+  const uint32_t* pair;
+  const uint32_t* cell;
+  const unsigned long long* count;   // device count (requests) ...
+  const unsigned long long* count2;  // ... or pair_off[n_pairs] (emitted rows)
+  int64_t cap;
+};
+
+__device__ __forceinline__ int64_t cell_list_len(const CellList& cl) {
+  const unsigned long long c = cl.count ? *cl.count : *cl.count2;
+  return (int64_t)min((unsigned long long)cl.cap, c);
+}
+
+constexpr int kPwRootThreads = 128;
+constexpr int kPwCellsPerLaunch = 16384;
+
+// grid: (roots / kPwRootThreads, cells in this batch)
+__global__ void __launch_bounds__(kPwRootThreads)
+pw_roots_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
+                const double* __restrict__ h, const double* __restrict__ scores, CellList cl,
+                int64_t first, const PwPlan* __restrict__ plan, double* __restrict__ vals) {
+  const int64_t c = first + blockIdx.y;
+  if (c >= cell_list_len(cl)) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= plan->n_roots) return;
+  const int p = (int)cl.pair[c];
+  const uint32_t cell = cl.cell[c];
+  const PairConst pc = pcs[p];
+  const CellCost cc{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
+  const int node = plan->root[r];
+  vals[(int64_t)blockIdx.y * kPwPlanNodes + node] =
+      pw_subtree(h, scores + (int64_t)pc.slot * g.n, plan->off[node], plan->len[node], cc);
+}
+
+__global__ void pw_combine_kernel(CellList cl, int64_t first, const PwPlan* __restrict__ plan,
+                                  double* __restrict__ vals, double dn,
+                                  double* __restrict__ out_fid) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = first + j;
+  if (j >= kPwCellsPerLaunch || c >= cell_list_len(cl)) return;
+  double* v = vals + j * kPwPlanNodes;
+  for (int i = plan->n_nodes - 1; i >= 0; --i) {
+    const int ch = plan->child[i];
+    if (ch >= 0) v[i] = __dadd_rn(v[ch], v[ch + 1]);
+  }
+  out_fid[c] = __ddiv_rn(v[0], dn);
+}
+
+
 __global__ void __launch_bounds__(kPwThreads)
 exact_requests_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
                       const double* __restrict__ h, const double* __restrict__ scores,
@@ -1006,7 +1057,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 
 struct Layout {
   size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
-      counters, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
+      counters, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1039,6 +1090,9 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
   L.req[0] = take(4 * ecap); L.req[1] = take(4 * ecap); L.req[2] = take(8 * ecap);
   L.counters = take(8 * 8);
+  L.pwplan = take(sizeof(PwPlan));
+  const int64_t pw_batch = std::min<int64_t>(std::max(ecap, out_cap), kPwCellsPerLaunch);
+  L.pwvals = take(8 * (int64_t)kPwPlanNodes * pw_batch);
   const int64_t n_cw = ceil_div((cells + 31) / 32, 256) * n_pairs;    // emit chunks
   L.pair_rows = take(4 * n_cw);
   L.chunk_off = take(8 * (n_cw + 1));
@@ -1113,6 +1167,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* req_cell = (uint32_t*)P(L.req[1]);
   double* req_fid = (double*)P(L.req[2]);
   unsigned long long* counters = (unsigned long long*)P(L.counters);
+  PwPlan* pwplan = (PwPlan*)P(L.pwplan);
+  double* pwvals = (double*)P(L.pwvals);
   uint32_t* chunk_rows = (uint32_t*)P(L.pair_rows);
   unsigned long long* chunk_off = (unsigned long long*)P(L.chunk_off);
   unsigned long long* ctsum = (unsigned long long*)P(L.ctsum);
@@ -1131,6 +1187,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
+  int launches = 23;   // fixed kernels below; batched emulation adds 2 per batch
+  pw_plan_kernel<<<1, 1, 0, st>>>(n, pwplan);
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
@@ -1165,9 +1223,16 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_LAUNCH_CHECK();
   partners_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, un, grp, boff,
                                            reqbm, req_pair, req_cell, exact_cap, counters);
-  exact_requests_kernel<<<kNumSMs * 2, kPwThreads, 0, st>>>(g, pcs, thr_unique, h, scores,
-                                                            counters, exact_cap, req_pair,
-                                                            req_cell, req_fid);
+  {
+    const CellList cl{req_pair, req_cell, counters + 2, nullptr, exact_cap};
+    const int64_t batch = exact_cap < kPwCellsPerLaunch ? exact_cap : kPwCellsPerLaunch;
+    for (int64_t first = 0; first < exact_cap; first += kPwCellsPerLaunch, launches += 2) {
+      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)batch), kPwRootThreads, 0,
+                        st>>>(g, pcs, thr_unique, h, scores, cl, first, pwplan, pwvals);
+      pw_combine_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(cl, first, pwplan, pwvals,
+                                                                        (double)n, req_fid);
+    }
+  }
   sort_requests_kernel<<<1, 1024, 0, st>>>(counters, exact_cap, cells, req_pair, req_cell,
                                            req_fid);
   resolve_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, exact_cap, un,
@@ -1190,15 +1255,24 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   emit_rows_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(
       g, pcs, kept, words_per_pair, n_chunks, chunk_off, out_cap, out);
   if (exact_fid) {
-    exact_rows_kernel<<<kNumSMs * 2, kPwThreads, 0, st>>>(g, pcs, thr_unique, h, scores,
-                                                          pair_off, n_pairs, out_cap, out);
+    // every emitted row; out_cap bounds the batches launched (rows beyond the
+    // device row count exit immediately)
+    const CellList cl{reinterpret_cast<const uint32_t*>(out_pair), row_cell, nullptr,
+                      pair_off + n_pairs, out_cap};
+    const int64_t batch = out_cap < kPwCellsPerLaunch ? out_cap : kPwCellsPerLaunch;
+    for (int64_t first = 0; first < out_cap; first += kPwCellsPerLaunch, launches += 2) {
+      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)batch), kPwRootThreads, 0,
+                        st>>>(g, pcs, thr_unique, h, scores, cl, first, pwplan, pwvals);
+      pw_combine_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(cl, first, pwplan, pwvals,
+                                                                        (double)n, out_fid);
+    }
   } else {
     patch_rows_kernel<<<(unsigned)ceil_div(exact_cap, 256), 256, 0, st>>>(
         counters, exact_cap, req_pair, req_cell, req_fid, pair_off, out_cap, out);
   }
   finish_stats_kernel<<<1, 1, 0, st>>>(counters, cand_cap, exact_cap, exact_cap, stats);
   HADIS_LAUNCH_CHECK();
-  hadis_count_launches(24);
+  hadis_count_launches(exact_fid ? launches - 1 : launches);
   return HADIS_OK;
 }
 

@@ -161,7 +161,7 @@ extern "C" int hadis_hfix_shift(int64_t n) {
   int bits = 0;
   while ((n >> bits) != 0) ++bits;
   int shift = 63 - bits;
-  return shift > 62 ? 62 : shift;
+  return shift > 48 ? 48 : shift;   // <= 48-bit hardness fixed point (3 x 16-bit K1 limbs)
 }
 
 extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_light,

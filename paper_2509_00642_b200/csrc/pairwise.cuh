@@ -146,4 +146,48 @@ __device__ double pw_block_sum(const double* __restrict__ h, const double* __res
   return total;
 }
 
+// ---------------------------------------------------------------------------
+// Many-CTA form for batches of cells over large n: the top of the recursion
+// (shared by every cell, it depends only on n) is expanded once into a node
+// table; a 2-D grid (subtree roots x cells) sums every root subtree, and one
+// thread per cell folds the top tree.  Same association order as numpy.
+
+constexpr int kPwPlanNodes = 1024;
+constexpr int kPwPlanRoots = 512;
+
+struct PwPlan {
+  int n_nodes, n_roots;
+  int64_t off[kPwPlanNodes];
+  int64_t len[kPwPlanNodes];
+  int32_t child[kPwPlanNodes];   // left child index (right = +1) or -1 for a root
+  int32_t root[kPwPlanNodes];    // node index of the r-th root
+};
+
+__global__ void pw_plan_kernel(int64_t n, PwPlan* plan) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  plan->off[0] = 0;
+  plan->len[0] = n;
+  plan->child[0] = -1;
+  int count = 1, expanded = 0;
+  for (int i = 0; i < count; ++i) {
+    if (count - expanded >= kPwPlanRoots || count + 2 > kPwPlanNodes) break;
+    if (plan->len[i] <= kPwBlock) continue;
+    const int64_t half = pw_split(plan->len[i]);
+    plan->child[i] = count;
+    plan->off[count] = plan->off[i];
+    plan->len[count] = half;
+    plan->child[count] = -1;
+    plan->off[count + 1] = plan->off[i] + half;
+    plan->len[count + 1] = plan->len[i] - half;
+    plan->child[count + 1] = -1;
+    count += 2;
+    ++expanded;
+  }
+  int r = 0;
+  for (int i = 0; i < count; ++i)
+    if (plan->child[i] < 0) plan->root[r++] = i;
+  plan->n_nodes = count;
+  plan->n_roots = r;
+}
+
 }  // namespace hadis

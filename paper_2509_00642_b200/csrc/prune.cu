@@ -39,7 +39,7 @@ tile_sort_kernel(const double* __restrict__ lat, const double* __restrict__ qual
     const int64_t g = base + j;
     if (g < n) {
       sa[j] = order_key(lat[g]);
-      sb[j] = order_key(qual[g]);
+      sb[j] = qual ? order_key(qual[g]) : 0ull;
       si[j] = (uint32_t)g;
     } else {
       sa[j] = ~0ull; sb[j] = ~0ull; si[j] = 0xffffffffu;
@@ -137,13 +137,46 @@ keep_compact_kernel(const unsigned long long* __restrict__ kb, const uint32_t* _
   if (threadIdx.x == blockDim.x - 1) out_count[0] = (int64_t)part_cnt[blockDim.x - 1];
 }
 
+// Sort n (k1, k2, index) keys ascending (k2 may be null); ws must hold
+// sort_workspace_bytes(n).  *sorted_idx / *sorted_k2 point into ws on return.
+size_t sort_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 20 + 255) & ~(size_t)255); }
+
+int sort_keys(const double* k1, const double* k2, int64_t n, void* workspace, cudaStream_t st,
+              const uint32_t** sorted_idx, const unsigned long long** sorted_k2) {
+  char* ws = (char*)workspace;
+  unsigned long long* a0 = (unsigned long long*)ws;
+  unsigned long long* b0 = a0 + n;
+  uint32_t* i0 = (uint32_t*)(b0 + n);
+  unsigned long long* a1 = (unsigned long long*)(ws + (((size_t)n * 20 + 255) & ~(size_t)255));
+  unsigned long long* b1 = a1 + n;
+  uint32_t* i1 = (uint32_t*)(b1 + n);
+  const int64_t tiles = ceil_div(n, kTile);
+  tile_sort_kernel<<<(unsigned)tiles, kPruneThreads, 0, st>>>(k1, k2, n, a0, b0, i0);
+  HADIS_LAUNCH_CHECK();
+  int launches = 1;
+  bool in0 = true;
+  for (int64_t run = kTile; run < n; run <<= 1) {
+    int64_t grid = ceil_div(n, 256);
+    if (grid > kNumSMs * 8) grid = kNumSMs * 8;
+    if (in0) merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a0, b0, i0, n, run, a1, b1, i1);
+    else merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a1, b1, i1, n, run, a0, b0, i0);
+    HADIS_LAUNCH_CHECK();
+    ++launches;
+    in0 = !in0;
+  }
+  hadis_count_launches(launches);
+  *sorted_idx = in0 ? i0 : i1;
+  if (sorted_k2) *sorted_k2 = in0 ? b0 : b1;
+  return HADIS_OK;
+}
+
 }  // namespace hadis
 
 using namespace hadis;
 
 extern "C" size_t hadis_pareto_workspace_bytes(int64_t n) {
   if (n <= 0) return 0;
-  return 2 * (((size_t)n * 20 + 255) & ~(size_t)255);
+  return sort_workspace_bytes(n);
 }
 
 extern "C" int hadis_pareto_prune(const double* lat, const double* qual, int64_t n,
@@ -153,29 +186,12 @@ extern "C" int hadis_pareto_prune(const double* lat, const double* qual, int64_t
     return HADIS_ERR_ARG;
   if (workspace_bytes < hadis_pareto_workspace_bytes(n)) return HADIS_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
-  char* ws = (char*)workspace;
-  unsigned long long* a0 = (unsigned long long*)ws;
-  unsigned long long* b0 = a0 + n;
-  uint32_t* i0 = (uint32_t*)(b0 + n);
-  unsigned long long* a1 = (unsigned long long*)(ws + (((size_t)n * 20 + 255) & ~(size_t)255));
-  unsigned long long* b1 = a1 + n;
-  uint32_t* i1 = (uint32_t*)(b1 + n);
-  const int64_t tiles = ceil_div(n, kTile);
-  tile_sort_kernel<<<(unsigned)tiles, kPruneThreads, 0, st>>>(lat, qual, n, a0, b0, i0);
+  const uint32_t* idx = nullptr;
+  const unsigned long long* kb = nullptr;
+  const int rc = sort_keys(lat, qual, n, workspace, st, &idx, &kb);
+  if (rc != HADIS_OK) return rc;
+  keep_compact_kernel<<<1, kPruneThreads, 0, st>>>(kb, idx, n, out_idx, out_count);
   HADIS_LAUNCH_CHECK();
-  bool in0 = true;
-  for (int64_t run = kTile; run < n; run <<= 1) {
-    int64_t grid = ceil_div(n, 256);
-    if (grid > kNumSMs * 8) grid = kNumSMs * 8;
-    if (in0) merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a0, b0, i0, n, run, a1, b1, i1);
-    else merge_pass_kernel<<<(unsigned)grid, 256, 0, st>>>(a1, b1, i1, n, run, a0, b0, i0);
-    HADIS_LAUNCH_CHECK();
-    hadis_count_launches(1);
-    in0 = !in0;
-  }
-  keep_compact_kernel<<<1, kPruneThreads, 0, st>>>(in0 ? b0 : b1, in0 ? i0 : i1, n, out_idx,
-                                                   out_count);
-  HADIS_LAUNCH_CHECK();
-  hadis_count_launches(2);
+  hadis_count_launches(1);
   return HADIS_OK;
 }

@@ -264,7 +264,7 @@ class GridProfiler:
     ``run`` profiles one threshold grid; ``launch``/``finish`` split it into an
     asynchronous enqueue and a synchronising check for pipelined callers."""
 
-    def __init__(self, pool, h, scores, device=None):
+    def __init__(self, pool, h, scores, device=None, layout="sorted"):
         torch = _lib.torch_cuda()
         self.torch = torch
         self.pool = list(pool)
@@ -283,6 +283,30 @@ class GridProfiler:
         self.shift = self.lib.hadis_hfix_shift(self.n)
         self._ws = None
         self._plans = {}
+        if layout not in ("sorted", "original"):
+            raise ValueError("layout must be 'sorted' or 'original'")
+        self.layout = layout
+        self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if layout == "sorted":
+            self.ingest()
+
+    def ingest(self, stream=None):
+        """Record-store layout: hardness-sorted copies of h and the score rows
+        (hadis_records_sort).  K1 then reads each threshold row as a contiguous
+        run; the original-order arrays stay for the exact-fidelity emulation."""
+        torch = self.torch
+        L = int(self.scores.shape[0])
+        self.hs = torch.empty_like(self.h)
+        self.ss = torch.empty_like(self.scores)
+        ws_bytes = self.lib.hadis_records_workspace_bytes(self.n)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
+        p = _lib.ptr
+        _lib.check(self.lib.hadis_records_sort(p(self.h), p(self.scores), self.n, L, p(self.hs),
+                                               p(self.ss), None, p(self.bad), p(ws), ws_bytes,
+                                               _lib.stream_handle(stream)), "hadis_records_sort")
+        self._k1_ws = torch.empty(max(1, self.lib.hadis_bin_hist_sorted_workspace_bytes(8192)),
+                                  dtype=torch.uint8, device=self.device)
+        del ws
 
     def plan(self, thresholds=THRESHOLD_GRID, pairs=None) -> ProfilePlan:
         key = (tuple(float(t) for t in thresholds), None if pairs is None else tuple(pairs))
@@ -306,14 +330,20 @@ class GridProfiler:
         state = dict(plan=plan, exact_fid=exact_fid, stream=stream,
                      cnt=torch.empty(bins, dtype=torch.int32, device=dev),
                      hsum=torch.empty(bins, dtype=torch.int64, device=dev),
-                     bad=torch.empty(1, dtype=torch.int32, device=dev),
                      scores=self.scores[plan.slot0:plan.slot0 + plan.n_light])
         p = _lib.ptr
         rec = (lambda i: events[i].record(stream)) if events is not None else (lambda i: None)
         rec(0)
-        _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
-                                           p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
-                                           p(state["hsum"]), p(state["bad"]), st), "hadis_bin_hist")
+        if self.layout == "sorted":
+            ss = self.ss[plan.slot0:plan.slot0 + plan.n_light]
+            _lib.check(self.lib.hadis_bin_hist_sorted(
+                p(self.hs), p(ss), self.n, plan.n_light, p(plan.d_u), plan.U, self.shift,
+                p(state["cnt"]), p(state["hsum"]), p(self._k1_ws), self._k1_ws.numel(), st),
+                "hadis_bin_hist_sorted")
+        else:
+            _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
+                                               p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
+                                               p(state["hsum"]), p(self.bad), st), "hadis_bin_hist")
         rec(1)
         _lib.check(self.lib.hadis_hist_scan(p(state["cnt"]), p(state["hsum"]), plan.n_light,
                                             plan.U, st), "hadis_hist_scan")
@@ -356,7 +386,7 @@ class GridProfiler:
         plan = state["plan"]
         for _ in range(6):
             stats = state["stats"].cpu().tolist()
-            if int(state["bad"].item()):
+            if int(self.bad.item()):
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW] == 0:
                 break

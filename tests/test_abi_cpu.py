@@ -32,7 +32,7 @@ def test_library_pure_host_calls():
     assert lib.hadis_abi_version() == 1
     assert lib.hadis_status_string(5) == b"fallback: no serveable rows"
     assert lib.hadis_hfix_shift(10_000_000) == 63 - 24
-    assert lib.hadis_hfix_shift(1) == 62
+    assert lib.hadis_hfix_shift(1) == 48
     assert lib.hadis_frontier_workspace_bytes(6, 256, 1 << 20, 2048, 1 << 20) > 0
     assert lib.hadis_pareto_workspace_bytes(0) == 0
 

@@ -250,3 +250,22 @@ def test_c2_scale_properties(gpu_device):
                                                  lt.latency_s[1], hv.latency_s[1], r.theta, r.tau)
         assert (r.r_light, r.r_heavy, r.mean_latency_s) == (rl, rh, lat)
         assert math.isclose(r.fidelity_cost, fid, rel_tol=1e-9)
+
+
+@pytest.mark.parametrize("layout", ["sorted", "original"])
+def test_k1_layouts_agree(gpu_device, layout):
+    """Both K1 paths (hardness-sorted record store / original order with L2
+    atomics) give the same table as the oracle."""
+    rng = np.random.default_rng(99)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    n = 50_000
+    h = rng.choice(np.round(rng.uniform(0.0, 1.0, 500), 3), n)
+    noise = rng.normal(0.0, 0.08, n)
+    thr = tuple(i / 47 for i in range(48))
+    prof = GridProfiler(pool, h, light_scores(pool, h, noise), layout=layout)
+    from paper_2509_00642_b200.profiler import rows_from_device
+    got = [(r.light_id, r.heavy_id, r.theta, r.tau, r.r_light, r.r_heavy, r.fidelity_cost,
+            r.mean_latency_s) for r in rows_from_device(prof.run(thr), pool, thr)]
+    want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
+    assert_rows_close(got, want)
