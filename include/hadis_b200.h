@@ -61,36 +61,41 @@ int64_t hadis_kernel_launches(void);
 int hadis_hfix_shift(int64_t n);
 
 /* Record-store ingest: order records by hardness (ties by original index) and
- * gather the n_rows score rows (row stride n) into the same order.  perm (may
- * be NULL) receives the original index of each sorted position; bad_records
- * counts hardness values that are NaN or outside [0, 1]. */
+ * gather the n_rows score rows (row stride n) into the same order; hfix_sorted
+ * receives floor(h * 2^hfix_shift) of each sorted record.  perm (may be NULL)
+ * receives the original index of each sorted position; bad_records counts
+ * hardness values that are NaN or outside [0, 1]. */
 size_t hadis_records_workspace_bytes(int64_t n);
 int hadis_records_sort(const double* h, const double* scores, int64_t n, int32_t n_rows,
-                       double* h_sorted, double* scores_sorted, uint32_t* perm,
-                       uint32_t* bad_records, void* workspace, size_t workspace_bytes,
-                       void* stream);
-
-/* K1 on a hardness-sorted record store (profiler.py:138, 145-150): same
- * histogram as hadis_bin_hist, built without global atomics -- each row of
- * equal bh is a contiguous run of sorted records, so one CTA per (row chunk,
- * light model) accumulates in shared memory and stores the row. */
-size_t hadis_bin_hist_sorted_workspace_bytes(int32_t n_unique);
-int hadis_bin_hist_sorted(const double* h_sorted, const double* scores_sorted, int64_t n,
-                          int32_t n_light, const double* thr_unique, int32_t n_unique,
-                          int32_t hfix_shift, uint32_t* hist_cnt, uint64_t* hist_hsum,
-                          void* workspace, size_t workspace_bytes, void* stream);
+                       int32_t hfix_shift, double* h_sorted, uint64_t* hfix_sorted,
+                       double* scores_sorted, uint32_t* perm, uint32_t* bad_records,
+                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* K1 -- bin + 2-D histogram (profiler.py:138, 145-150: bypass h > theta,
- * reject score < tau).  For every record q and light model l:
+ * reject score < tau), records in any order.  For every record q and light
+ * model l:
  *   bh = #{u < h[q]},  bs = #{u <= s_l[q]}   (u = sorted distinct thresholds)
  *   hist_cnt [l][bh][bs] += 1 ;  hist_hsum[l][bh][bs] += floor(h[q] * 2^shift)
  * scores: n_light rows of n float64 (row stride n).  Histograms have
- * (n_unique+1)^2 cells per light model and are zeroed by this call.
+ * (n_unique+1)^2 cells per light model and are zeroed by this call; L2
+ * integer atomics (or shared-memory privatisation for small grids).
  * bad_records (device uint32) counts records with h outside [0, 1] / NaN. */
 int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_light,
                    const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
                    uint32_t* hist_cnt, uint64_t* hist_hsum, uint32_t* bad_records,
                    void* stream);
+
+/* K1 on a hardness-sorted record store (profiler.py:138, 145-150): same
+ * histogram as hadis_bin_hist, built without global atomics -- each row of
+ * equal bh is a contiguous run of sorted records, so one CTA per (row chunk,
+ * light model) accumulates in shared memory and stores the row.  Supports up
+ * to 2047 distinct thresholds (hadis_bin_hist covers larger grids). */
+size_t hadis_bin_hist_sorted_workspace_bytes(int64_t n, int32_t n_unique);
+int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfix_sorted,
+                          const double* scores_sorted, int64_t n, int32_t n_light,
+                          const double* thr_unique, int32_t n_unique, uint32_t* hist_cnt,
+                          uint64_t* hist_hsum, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* K2 -- in-place 2-D inclusive prefix sums of the K1 histograms:
  *   cnt[l][k][t] = #{q : bh(q) <= k, bs_l(q) <= t}  (and the same for hsum). */

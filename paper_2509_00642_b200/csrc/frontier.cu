@@ -117,6 +117,33 @@ __device__ __forceinline__ void cell_numerators(const Grid& g, const PairConst& 
   *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, (double)nH), __dmul_rn(pc.bl, (double)(n - nH))), hterm);
 }
 
+// Per-(light slot, k, t) integer statistics, shared by every heavy partner.
+struct CellInts {
+  uint32_t Rk, nH;       // records kept by the light stage; heavy-served records
+  uint64_t SH, SL;       // fixed-point hardness sums of heavy / light-served records
+};
+
+__device__ __forceinline__ CellInts cell_ints(const Grid& g, const uint32_t* C, const uint64_t* Sh,
+                                             int k, int t) {
+  const int64_t rk = (int64_t)k * g.B1;
+  CellInts c;
+  c.Rk = C[rk + g.U];
+  const uint64_t Htot = Sh[(int64_t)g.U * g.B1 + g.U];
+  c.nH = ((uint32_t)g.n - c.Rk) + C[rk + t];
+  c.SH = (Htot - Sh[rk + g.U]) + Sh[rk + t];
+  c.SL = Htot - c.SH;
+  return c;
+}
+
+__device__ __forceinline__ void numerators_of(const Grid& g, const PairConst& pc, const CellInts& c,
+                                              double* x, double* S) {
+  *x = __dadd_rn(__dmul_rn((double)c.Rk, pc.Ll), __dmul_rn((double)c.nH, pc.Lh));
+  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)c.SH),
+                                           __dmul_rn(pc.pl, (double)c.SL)), g.inv_scale);
+  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, (double)c.nH),
+                           __dmul_rn(pc.bl, (double)((uint32_t)g.n - c.nH))), hterm);
+}
+
 // bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
 __device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, double x) {
   double b = floor(__dmul_rn(__dadd_rn(x, -pc.lo_x), pc.scale_x));
@@ -223,21 +250,18 @@ row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
     if (k > 0 && first_pos[k] < first_pos[k - 1]) s_unsorted = 1;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  *sorted = !s_unsorted;
-  int start = 0;
-  for (int k = 0; k <= U; ++k) {
-    if (k == U || (k > 0 && s_R[k] != s_R[k - 1])) {
-      int best = start;                        // close class [start, k)
-      for (int j = start + 1; j < k; ++j)
-        if (first_pos[j] < first_pos[best]) best = j;
-      for (int j = start; j < k; ++j) {
-        row_rep[j] = best;
-        pk[j] = start - 1;
-        row_start[j] = j == start;
-      }
-      start = k;
-    }
+  if (threadIdx.x == 0) *sorted = !s_unsorted;
+  // classes are runs of equal R; each rank walks to its run's ends
+  for (int k = threadIdx.x; k < U; k += blockDim.x) {
+    int a = k, b = k + 1;
+    while (a > 0 && s_R[a - 1] == s_R[k]) --a;
+    while (b < U && s_R[b] == s_R[k]) ++b;
+    int best = a;
+    for (int j = a + 1; j < b; ++j)
+      if (first_pos[j] < first_pos[best]) best = j;
+    row_rep[k] = best;
+    pk[k] = a - 1;
+    row_start[k] = k == a;
   }
 }
 
@@ -245,20 +269,37 @@ row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
 
 constexpr int kCellThreads = 256;
 
+// Pairs sharing a light slot are contiguous ("groups"); a thread loads one
+// (slot, k, t) cell's integer statistics once and evaluates every heavy
+// partner of the group.  grid: (cell tiles, group upper bound), x fastest, so
+// one light model's prefix table stays L2-resident while its pairs run.
+__global__ void group_kernel(const int32_t* __restrict__ pair_slot, int n_pairs,
+                             int32_t* __restrict__ group_p0, int32_t* __restrict__ n_groups) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int ng = 0;
+  for (int p = 0; p < n_pairs; ++p)
+    if (p == 0 || pair_slot[p] != pair_slot[p - 1]) group_p0[ng++] = p;
+  group_p0[ng] = n_pairs;
+  *n_groups = ng;
+}
+
 __global__ void __launch_bounds__(kCellThreads)
-bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
-                  unsigned long long* __restrict__ bmin) {
-  const int64_t cells = (int64_t)g.U * g.U;
-  const int64_t total = cells * n_pairs;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int p = (int)(i / cells);
-    const int64_t c = i - (int64_t)p * cells;
-    const int k = (int)(c / g.U), t = (int)(c % g.U);
+bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
+                  const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
+  const int grp = blockIdx.y;
+  if (grp >= *n_groups) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)g.U * g.U) return;
+  const int k = (int)(c / g.U), t = (int)(c % g.U);
+  const int p0 = group_p0[grp], p1 = group_p0[grp + 1];
+  const int slot = pcs[p0].slot;
+  const uint32_t* C = slot_cnt(g, slot);
+  if (!class_start(g, C, k, t)) return;   // exact duplicate of an earlier cell
+  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
+  for (int p = p0; p < p1; ++p) {
     const PairConst pc = pcs[p];
-    if (!class_start(g, slot_cnt(g, pc.slot), k, t)) continue;   // exact duplicate
     double x, S;
-    cell_numerators(g, pc, k, t, &x, &S);
+    numerators_of(g, pc, ci, &x, &S);
     const int b = bucket_of_x(pc, g.nbuckets, x);
     atomicMin(&bmin[(int64_t)p * g.nbuckets + b], (unsigned long long)order_key(S));
   }
@@ -334,49 +375,52 @@ struct Cands {
   double* fid;
 };
 
+// Two passes over the cells: COUNT candidates per (pair, bucket), scan the
+// counts into bucket offsets, then WRITE every candidate straight into its
+// bucket's segment -- no global candidate counter, no separate scatter.
+template <bool kWrite>
 __global__ void __launch_bounds__(kCellThreads)
-filter_kernel(Grid g, const PairConst* __restrict__ pcs, int n_pairs,
-              const double* __restrict__ gpre, uint32_t* __restrict__ bcnt, Cands raw,
-              int64_t cap, unsigned long long* __restrict__ counters) {
-  const int64_t cells = (int64_t)g.U * g.U;
-  const int64_t total = cells * n_pairs;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
+filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
+              const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
+              uint32_t* __restrict__ bcnt, const unsigned long long* __restrict__ boff,
+              uint32_t* __restrict__ bcur, Cands grp, int64_t cap) {
+  const int gi = blockIdx.y;
+  if (gi >= *n_groups) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)g.U * g.U) return;
+  const int k = (int)(c / g.U), t = (int)(c % g.U);
+  const int p0 = group_p0[gi], p1 = group_p0[gi + 1];
+  const int slot = pcs[p0].slot;
+  const uint32_t* C = slot_cnt(g, slot);
+  if (!class_start(g, C, k, t)) return;
+  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
   const double dn = (double)g.n;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool take = false;
-    int p = 0, b = 0, k = 0, t = 0;
-    double x = 0.0, S = 0.0;
-    if (i < total) {
-      p = (int)(i / cells);
-      const int64_t c = i - (int64_t)p * cells;
-      k = (int)(c / g.U);
-      t = (int)(c % g.U);
-      const PairConst pc = pcs[p];
-      if (class_start(g, slot_cnt(g, pc.slot), k, t)) {
-        cell_numerators(g, pc, k, t, &x, &S);
-        b = bucket_of_x(pc, g.nbuckets, x);
-        take = S <= gpre[(int64_t)p * g.nbuckets + b] + pc.delta2_S;
-      }
+  uint32_t rep = 0xffffffffu;
+  for (int p = p0; p < p1; ++p) {
+    const PairConst pc = pcs[p];
+    double x, S;
+    numerators_of(g, pc, ci, &x, &S);
+    const int b = bucket_of_x(pc, g.nbuckets, x);
+    const int64_t key = (int64_t)p * g.nbuckets + b;
+    if (!(S <= gpre[key] + pc.delta2_S)) continue;
+    if (!kWrite) {
+      atomicAdd(&bcnt[key], 1u);
+      continue;
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (!mask) continue;
-    unsigned long long slot0 = 0;
-    if (lane == 0) slot0 = atomicAdd(&counters[0], (unsigned long long)__popc(mask));
-    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-    if (take) {
-      const int64_t at = (int64_t)slot0 + __popc(mask & ((1u << lane) - 1u));
-      atomicAdd(&bcnt[(int64_t)p * g.nbuckets + b], 1u);
-      if (at < cap) {
-        raw.pair[at] = (uint32_t)p;
-        raw.cell[at] = rep_cell(g, slot_cnt(g, pcs[p].slot), k, t, true);
-        raw.bucket[at] = (uint32_t)b;
-        raw.lat[at] = __ddiv_rn(x, dn);
-        raw.fid[at] = __ddiv_rn(S, dn);
-      }
-    }
+    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
+    if (at >= cap) continue;
+    if (rep == 0xffffffffu) rep = rep_cell(g, C, k, t, true);
+    grp.pair[at] = (uint32_t)p;
+    grp.cell[at] = rep;
+    grp.bucket[at] = (uint32_t)b;
+    grp.lat[at] = __ddiv_rn(x, dn);
+    grp.fid[at] = __ddiv_rn(S, dn);
   }
+}
+
+__global__ void candidates_total_kernel(const unsigned long long* __restrict__ total,
+                                        unsigned long long* __restrict__ counters) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = *total;
 }
 
 // ---------------------------------------------- F4: offsets (exclusive scan)
@@ -456,27 +500,6 @@ tile_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
   }
 }
 
-// ------------------------------------------------------------ F5: scatter
-
-__global__ void scatter_kernel(Cands raw, const unsigned long long* __restrict__ counters,
-                               int64_t cap, int nbuckets,
-                               const unsigned long long* __restrict__ boff,
-                               uint32_t* __restrict__ bcur, Cands grp) {
-  if ((int64_t)counters[0] > cap) return;   // overflow: host reruns with more room
-  const int64_t m = (int64_t)counters[0];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const int64_t key = (int64_t)raw.pair[i] * nbuckets + raw.bucket[i];
-    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
-    if (at >= cap) continue;
-    grp.pair[at] = raw.pair[i];
-    grp.cell[at] = raw.cell[i];
-    grp.bucket[at] = raw.bucket[i];
-    grp.lat[at] = raw.lat[i];
-    grp.fid[at] = raw.fid[i];
-  }
-}
-
 // --------------------------------------------------------------- F6: decide
 
 struct Uncertain {
@@ -536,27 +559,28 @@ __global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     const PairConst pc = pcs[p];
     const int64_t idx = grid_index(g, k, t);
     bool killed = false, unsure = false;
-
-    // heavy-set twin with more bypass: equal fidelity, strictly lower latency
-    const int kp = g.pk[k];
-    if (kp >= 0) {
-      const uint32_t* C = slot_cnt(g, pc.slot);
-      const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
-      if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
-        const CellVal tw = eval_cell(g, pc, kp, t);
-        if (tw.lat < lat) {
-          killed = true;
-        } else if (tw.lat == lat) {
-          const uint32_t tc = rep_cell(g, C, kp, t);
-          if (grid_index(g, (int)(tc / g.U), (int)(tc % g.U)) < idx) killed = true;
+    // gpre holds numerators S; fl(S / n) is exactly the lower buckets' min fid*
+    const double G = __ddiv_rn(gpre[(int64_t)p * g.nbuckets + b], (double)g.n);
+    if (G < fid - pc.delta2) {
+      killed = true;
+    } else if (G <= fid + pc.delta2) {
+      // a lower-bucket cell is close: certain only if it is c's heavy-set twin
+      // with more bypass (equal fidelity, strictly lower latency)
+      unsure = true;
+      const int kp = g.pk[k];
+      if (kp >= 0) {
+        const uint32_t* C = slot_cnt(g, pc.slot);
+        const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
+        if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
+          const CellVal tw = eval_cell(g, pc, kp, t);
+          if (tw.lat < lat) {
+            killed = true;
+          } else if (tw.lat == lat) {
+            const uint32_t tc = rep_cell(g, C, kp, t);
+            if (grid_index(g, (int)(tc / g.U), (int)(tc % g.U)) < idx) killed = true;
+          }
         }
       }
-    }
-    if (!killed) {
-      // gpre holds numerators S; fl(S / n) is exactly that cell's fid*
-      const double G = __ddiv_rn(gpre[(int64_t)p * g.nbuckets + b], (double)g.n);
-      if (G < fid - pc.delta2) killed = true;
-      else if (G <= fid + pc.delta2) unsure = true;
     }
     if (!killed) {
       const int64_t key = (int64_t)p * g.nbuckets + b;
@@ -741,24 +765,6 @@ __global__ void pw_combine_kernel(CellList cl, int64_t first, const PwPlan* __re
   out_fid[c] = __ddiv_rn(v[0], dn);
 }
 
-
-__global__ void __launch_bounds__(kPwThreads)
-exact_requests_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
-                      const double* __restrict__ h, const double* __restrict__ scores,
-                      const unsigned long long* __restrict__ counters_ro, int64_t rcap,
-                      const uint32_t* __restrict__ req_pair, const uint32_t* __restrict__ req_cell,
-                      double* __restrict__ req_fid) {
-  __shared__ PwShared sh;
-  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
-  for (int64_t e = blockIdx.x; e < nr; e += gridDim.x) {
-    const int p = (int)req_pair[e];
-    const uint32_t cell = req_cell[e];
-    const PairConst pc = pcs[p];
-    CellCost c{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
-    const double sum = pw_block_sum(h, scores + (int64_t)pc.slot * g.n, g.n, c, sh);
-    if (threadIdx.x == 0) req_fid[e] = __ddiv_rn(sum, (double)g.n);
-  }
-}
 
 // ------------------------------------------- F10: sort requests by (pair, cell)
 
@@ -1009,25 +1015,6 @@ __global__ void patch_rows_kernel(const unsigned long long* __restrict__ counter
   if (lo < (int64_t)pair_off[p + 1] && lo < out_cap && out.cell[lo] == cell) out.fid[lo] = req_fid[i];
 }
 
-// F14: exact_fid mode -- numpy-exact fidelity for every emitted row
-__global__ void __launch_bounds__(kPwThreads)
-exact_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
-                  const double* __restrict__ h, const double* __restrict__ scores,
-                  const unsigned long long* __restrict__ pair_off, int n_pairs, int64_t out_cap,
-                  Rows out) {
-  __shared__ PwShared sh;
-  int64_t rows = (int64_t)pair_off[n_pairs];
-  if (rows > out_cap) rows = out_cap;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    const int p = out.pair[r];
-    const uint32_t cell = out.cell[r];
-    const PairConst pc = pcs[p];
-    CellCost c{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
-    const double sum = pw_block_sum(h, scores + (int64_t)pc.slot * g.n, g.n, c, sh);
-    if (threadIdx.x == 0) out.fid[r] = __ddiv_rn(sum, (double)g.n);
-  }
-}
-
 __global__ void finish_stats_kernel(const unsigned long long* counters, int64_t cap, int64_t ucap,
                                     int64_t rcap, int64_t* stats) {
   unsigned long long of = counters[4];
@@ -1056,8 +1043,8 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, raw[5], grp[5], kept, reqbm, un[3], req[3],
-      counters, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
+  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, grp[5], kept, reqbm, un[3], req[3],
+      counters, groups, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1081,8 +1068,6 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.bcnt = take(4 * pb);
   L.bcur = take(4 * pb);
   L.boff = take(8 * (pb + 1));
-  L.raw[0] = take(4 * cap); L.raw[1] = take(4 * cap); L.raw[2] = take(4 * cap);
-  L.raw[3] = take(8 * cap); L.raw[4] = take(8 * cap);
   L.grp[0] = take(4 * cap); L.grp[1] = take(4 * cap); L.grp[2] = take(4 * cap);
   L.grp[3] = take(8 * cap); L.grp[4] = take(8 * cap);
   L.kept = take(4 * words);
@@ -1090,6 +1075,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
   L.req[0] = take(4 * ecap); L.req[1] = take(4 * ecap); L.req[2] = take(8 * ecap);
   L.counters = take(8 * 8);
+  L.groups = take(4 * (n_pairs + 2));
   L.pwplan = take(sizeof(PwPlan));
   const int64_t pw_batch = std::min<int64_t>(std::max(ecap, out_cap), kPwCellsPerLaunch);
   L.pwvals = take(8 * (int64_t)kPwPlanNodes * pw_batch);
@@ -1156,8 +1142,6 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* bcnt = (uint32_t*)P(L.bcnt);
   uint32_t* bcur = (uint32_t*)P(L.bcur);
   unsigned long long* boff = (unsigned long long*)P(L.boff);
-  Cands raw{(uint32_t*)P(L.raw[0]), (uint32_t*)P(L.raw[1]), (uint32_t*)P(L.raw[2]),
-            (double*)P(L.raw[3]), (double*)P(L.raw[4])};
   Cands grp{(uint32_t*)P(L.grp[0]), (uint32_t*)P(L.grp[1]), (uint32_t*)P(L.grp[2]),
             (double*)P(L.grp[3]), (double*)P(L.grp[4])};
   uint32_t* kept = (uint32_t*)P(L.kept);
@@ -1167,6 +1151,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* req_cell = (uint32_t*)P(L.req[1]);
   double* req_fid = (double*)P(L.req[2]);
   unsigned long long* counters = (unsigned long long*)P(L.counters);
+  int32_t* n_groups = (int32_t*)P(L.groups);
+  int32_t* group_p0 = n_groups + 1;
   PwPlan* pwplan = (PwPlan*)P(L.pwplan);
   double* pwvals = (double*)P(L.pwvals);
   uint32_t* chunk_rows = (uint32_t*)P(L.pair_rows);
@@ -1187,8 +1173,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
-  int launches = 23;   // fixed kernels below; batched emulation adds 2 per batch
-  pw_plan_kernel<<<1, 1, 0, st>>>(n, pwplan);
+  int launches = 26;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
@@ -1199,17 +1184,21 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   const int64_t total_cells = cells * n_pairs;
   int64_t grid_cells = ceil_div(total_cells, kCellThreads);
   if (grid_cells > (int64_t)kNumSMs * 16) grid_cells = (int64_t)kNumSMs * 16;
-  bucket_min_kernel<<<(unsigned)grid_cells, kCellThreads, 0, st>>>(g, pcs, n_pairs, bmin);
+  const dim3 cell_grid((unsigned)ceil_div(cells, kCellThreads), (unsigned)n_pairs);
+  group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups);
+  bucket_min_kernel<<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, bmin);
   bucket_prefix_kernel<<<n_pairs, kScanThreads, 0, st>>>(bmin, nb, gpre);
-  filter_kernel<<<(unsigned)grid_cells, kCellThreads, 0, st>>>(g, pcs, n_pairs, gpre, bcnt, raw,
-                                                              cand_cap, counters);
+  filter_kernel<false><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
+                                                          boff, bcur, grp, cand_cap);
   {
     const int64_t tiles = ceil_div(pb, kScanTile);
     tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum);
     tile_offsets_kernel<<<1, kScanThreads, 0, st>>>(tsum, tiles, boff + pb);
     tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
   }
-  scatter_kernel<<<kNumSMs * 4, 256, 0, st>>>(raw, counters, cand_cap, nb, boff, bcur, grp);
+  candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
+  filter_kernel<true><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
+                                                         boff, bcur, grp, cand_cap);
   HADIS_LAUNCH_CHECK();
   decide_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, kept, un, exact_cap, reqbm, req_pair, req_cell,
@@ -1223,6 +1212,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_LAUNCH_CHECK();
   partners_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, un, grp, boff,
                                            reqbm, req_pair, req_cell, exact_cap, counters);
+  pw_plan_kernel<<<1, 256, 0, st>>>(n, pwplan, exact_fid ? nullptr : counters + 2);
   {
     const CellList cl{req_pair, req_cell, counters + 2, nullptr, exact_cap};
     const int64_t batch = exact_cap < kPwCellsPerLaunch ? exact_cap : kPwCellsPerLaunch;

@@ -163,31 +163,45 @@ struct PwPlan {
   int32_t root[kPwPlanNodes];    // node index of the r-th root
 };
 
-__global__ void pw_plan_kernel(int64_t n, PwPlan* plan) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  plan->off[0] = 0;
-  plan->len[0] = n;
-  plan->child[0] = -1;
-  int count = 1, expanded = 0;
-  for (int i = 0; i < count; ++i) {
-    if (count - expanded >= kPwPlanRoots || count + 2 > kPwPlanNodes) break;
-    if (plan->len[i] <= kPwBlock) continue;
-    const int64_t half = pw_split(plan->len[i]);
-    plan->child[i] = count;
-    plan->off[count] = plan->off[i];
-    plan->len[count] = half;
-    plan->child[count] = -1;
-    plan->off[count + 1] = plan->off[i] + half;
-    plan->len[count + 1] = plan->len[i] - half;
-    plan->child[count + 1] = -1;
-    count += 2;
-    ++expanded;
+// built in shared memory by one thread, then copied out by the block
+// skip (no exact cells needed) when *need is 0; need == nullptr: always build
+__global__ void __launch_bounds__(256) pw_plan_kernel(int64_t n, PwPlan* plan,
+                                                      const unsigned long long* need) {
+  __shared__ PwPlan sp;
+  if (need && *need == 0) return;
+  if (threadIdx.x == 0) {
+    sp.off[0] = 0;
+    sp.len[0] = n;
+    sp.child[0] = -1;
+    int count = 1, expanded = 0;
+    for (int i = 0; i < count; ++i) {
+      if (count - expanded >= kPwPlanRoots || count + 2 > kPwPlanNodes) break;
+      if (sp.len[i] <= kPwBlock) continue;
+      const int64_t half = pw_split(sp.len[i]);
+      sp.child[i] = count;
+      sp.off[count] = sp.off[i];
+      sp.len[count] = half;
+      sp.child[count] = -1;
+      sp.off[count + 1] = sp.off[i] + half;
+      sp.len[count + 1] = sp.len[i] - half;
+      sp.child[count + 1] = -1;
+      count += 2;
+      ++expanded;
+    }
+    int r = 0;
+    for (int i = 0; i < count; ++i)
+      if (sp.child[i] < 0) sp.root[r++] = i;
+    sp.n_nodes = count;
+    sp.n_roots = r;
   }
-  int r = 0;
-  for (int i = 0; i < count; ++i)
-    if (plan->child[i] < 0) plan->root[r++] = i;
-  plan->n_nodes = count;
-  plan->n_roots = r;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPwPlanNodes; i += blockDim.x) {
+    plan->off[i] = sp.off[i];
+    plan->len[i] = sp.len[i];
+    plan->child[i] = sp.child[i];
+    plan->root[i] = sp.root[i];
+  }
+  if (threadIdx.x == 0) { plan->n_nodes = sp.n_nodes; plan->n_roots = sp.n_roots; }
 }
 
 }  // namespace hadis

@@ -297,15 +297,17 @@ class GridProfiler:
         torch = self.torch
         L = int(self.scores.shape[0])
         self.hs = torch.empty_like(self.h)
+        self.hfs = torch.empty(self.n, dtype=torch.int64, device=self.device)
         self.ss = torch.empty_like(self.scores)
         ws_bytes = self.lib.hadis_records_workspace_bytes(self.n)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
         p = _lib.ptr
-        _lib.check(self.lib.hadis_records_sort(p(self.h), p(self.scores), self.n, L, p(self.hs),
-                                               p(self.ss), None, p(self.bad), p(ws), ws_bytes,
+        _lib.check(self.lib.hadis_records_sort(p(self.h), p(self.scores), self.n, L, self.shift,
+                                               p(self.hs), p(self.hfs), p(self.ss), None,
+                                               p(self.bad), p(ws), ws_bytes,
                                                _lib.stream_handle(stream)), "hadis_records_sort")
-        self._k1_ws = torch.empty(max(1, self.lib.hadis_bin_hist_sorted_workspace_bytes(8192)),
-                                  dtype=torch.uint8, device=self.device)
+        k1 = self.lib.hadis_bin_hist_sorted_workspace_bytes(self.n, 2047)
+        self._k1_ws = torch.empty(max(1, k1), dtype=torch.uint8, device=self.device)
         del ws
 
     def plan(self, thresholds=THRESHOLD_GRID, pairs=None) -> ProfilePlan:
@@ -334,10 +336,10 @@ class GridProfiler:
         p = _lib.ptr
         rec = (lambda i: events[i].record(stream)) if events is not None else (lambda i: None)
         rec(0)
-        if self.layout == "sorted":
+        if self.layout == "sorted" and plan.U < 2048:
             ss = self.ss[plan.slot0:plan.slot0 + plan.n_light]
             _lib.check(self.lib.hadis_bin_hist_sorted(
-                p(self.hs), p(ss), self.n, plan.n_light, p(plan.d_u), plan.U, self.shift,
+                p(self.hs), p(self.hfs), p(ss), self.n, plan.n_light, p(plan.d_u), plan.U,
                 p(state["cnt"]), p(state["hsum"]), p(self._k1_ws), self._k1_ws.numel(), st),
                 "hadis_bin_hist_sorted")
         else:
