@@ -211,10 +211,15 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())   # >1 rank per GPU only in gloo tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("HADIS_DIST_BACKEND", "nccl")   # gloo: multi-rank tests on 1 GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     pool, h, noise, scores = synth.records(cfg)
     pairs = pair_list(pool)
@@ -244,6 +249,12 @@ def run_ours(args, cfg):
             arrays = gather_rows(torch, dist, arrays, offset, dev)
         return arrays
 
+    ev_i = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_i[0].record(stream)
+    prof.ingest()
+    ev_i[1].record(stream)
+    torch.cuda.synchronize()
+    ingest_ms = ev_i[0].elapsed_time(ev_i[1])
     for _ in range(args.warmup):
         last = step()
     rows = int(last["pair"].shape[0])
@@ -284,6 +295,7 @@ def run_ours(args, cfg):
         if plan is not None:
             d_h.copy_(h_pin, non_blocking=True)
             d_sc[s0:s1].copy_(sc_pin, non_blocking=True)
+            prof.ingest()                     # record-store layout of the fresh records
         arrays = step()
         d2h = 0
         for f, v in arrays.items():           # D2H into pinned host buffers
@@ -297,7 +309,8 @@ def run_ours(args, cfg):
     barrier()
 
     # ---- max over ranks
-    vals = torch.tensor([ms, statistics.median(e2e_ms), ms_k1], dtype=torch.float64, device=dev)
+    vals = torch.tensor([ms, statistics.median(e2e_ms), ms_k1], dtype=torch.float64,
+                        device=dev if backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms_max, e2e_max, _ = vals.tolist()
@@ -317,6 +330,7 @@ def run_ours(args, cfg):
                        "parallelism": f"pair-shard x{world} + nccl all-gather" if world > 1
                        else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
             "table_build_ms": ms_max,
+            "ingest_ms": ingest_ms,
             "stage_ms": {"k1_bin_hist": ms_k1, "k2_scan": statistics.mean(k2),
                          "k3_k4_frontier": statistics.mean(k34)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

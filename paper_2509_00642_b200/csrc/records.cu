@@ -38,7 +38,15 @@ __global__ void gather_kernel(const double* __restrict__ h, const double* __rest
     h_sorted[i] = hq;
     hfix_sorted[i] = (unsigned long long)__dmul_rn(ok ? hq : 0.0, hscale);
     if (perm) perm[i] = q;
-    for (int l = 0; l < n_rows; ++l) s_sorted[(int64_t)l * n + i] = scores[(int64_t)l * n + q];
+    int l = 0;
+    for (; l + 8 <= n_rows; l += 8) {      // 8 random gathers in flight per thread
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = scores[(int64_t)(l + j) * n + q];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s_sorted[(int64_t)(l + j) * n + i] = v[j];
+    }
+    for (; l < n_rows; ++l) s_sorted[(int64_t)l * n + i] = scores[(int64_t)l * n + q];
   }
   if (my_bad) atomicAdd(bad, my_bad);
 }
@@ -73,15 +81,41 @@ row_plan_kernel(const double* __restrict__ hs, int64_t n, const double* __restri
   __syncthreads();
   for (int j = threadIdx.x; j <= kGuide; j += blockDim.x)
     guide[j] = (uint32_t)s_g[j] | ((uint32_t)s_g[j < kGuide ? j + 1 : kGuide] << 16);
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int k = 0; k <= U; ++k) {
-      item_off[k] = acc;
-      const int64_t len = rb[k + 1] - rb[k];
-      acc += len > 0 ? ceil_div(len, kRowChunk) : 0;
+  // item_off = exclusive prefix of per-row chunk counts (block-wide, chunked)
+  __shared__ int64_t s_carry;
+  __shared__ int64_t s_warp[32];
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base <= U; base += blockDim.x) {
+    const int k = base + threadIdx.x;
+    int64_t v = 0;
+    if (k <= U) { const int64_t len = rb[k + 1] - rb[k]; v = len > 0 ? ceil_div(len, kRowChunk) : 0; }
+    int64_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
     }
-    item_off[U + 1] = acc;
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t o = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += o;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    const int64_t excl = s_carry + (warp > 0 ? s_warp[warp - 1] : 0) + incl - v;
+    if (k <= U) item_off[k] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) item_off[U + 1] = s_carry;
 }
 
 // #{u <= s} via the guide table (s in [0, 1]) or binary search otherwise

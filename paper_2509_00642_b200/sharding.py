@@ -43,6 +43,8 @@ def gather_rows(torch, dist, arrays, pair_offset, device, group=None):
     """All-gather every rank's rows; returns dict of concatenated columns
     (float64 for doubles, int64 for ids) in canonical (rank = pair) order."""
     world = dist.get_world_size(group)
+    if dist.get_backend(group) == "gloo":      # gloo collectives run on host tensors
+        device = torch.device("cpu")
     local = pack_rows(torch, arrays, pair_offset, device)
     n_local = torch.tensor([local.shape[0]], dtype=torch.int64, device=device)
     counts = torch.empty(world, dtype=torch.int64, device=device)

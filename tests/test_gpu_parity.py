@@ -269,3 +269,20 @@ def test_k1_layouts_agree(gpu_device, layout):
             r.mean_latency_s) for r in rows_from_device(prof.run(thr), pool, thr)]
     want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
     assert_rows_close(got, want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_profile_equals_single(gpu_device, world):
+    """torchrun world ranks (gloo, sharing the box's GPU): pair-sharded
+    profiling + all-gather merge reproduces the 1-process table exactly."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HADIS_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                          "--nproc-per-node", str(world), os.path.join(root, "tools",
+                                                                       "check_sharded.py")],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "sharded OK" in out.stdout
