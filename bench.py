@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-allocation", action="store_true")
     return ap.parse_args()
 
 
@@ -342,6 +343,8 @@ def run_ours(args, cfg):
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
         }
+        if not args.no_allocation:
+            line["allocation_search"] = measure_allocation(torch, dev, args.steps)
         traffic = _ncu_traffic(cfg.name)
         if traffic:
             line["roofline"]["traffic"] = traffic
@@ -355,6 +358,64 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_allocation(torch, dev, steps, cpu_points=1):
+    """c5: 1000 (demand, SLO) re-plan points x the c2 Pareto table x every
+    worker split of W=8, on the device (hadis_solve_many), plus the reference
+    solve loop (oracle port) on a bounded sample of points."""
+    from types import SimpleNamespace
+
+    from oracle import planner as op
+    from paper_2509_00642_b200 import synth
+    from paper_2509_00642_b200.planner import DeviceRows
+    from paper_2509_00642_b200.profiler import GridProfiler
+    cfg = synth.CONFIGS["c2"]
+    pool, h, noise, scores = synth.records(cfg)
+    prof = GridProfiler(pool, h, scores, device=dev)
+    dt = prof.run(cfg.thresholds)
+    cat = cfg.catalog()
+    dr = DeviceRows.from_device_table(dt, pool, cat)
+    lams, slos, _ = synth.replan_points(1000)
+    P = len(lams)
+    d_lam = torch.tensor(lams, dtype=torch.float64, device=dev)
+    d_slo = torch.tensor(slos, dtype=torch.float64, device=dev)
+    d_w = torch.full((P,), cfg.workers, dtype=torch.int32, device=dev)
+    d_q = torch.zeros((P, len(cat.variants)), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        out = dr.launch(d_lam, d_slo, d_w, d_q, 1.5)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        out = dr.launch(d_lam, d_slo, d_w, d_q, 1.5)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    rows = dt.n_rows
+    combos = len(cat.batch_sizes) ** 2
+    # reference solve loop on a sample of points (host rows built once)
+    pair_ids = dt.pair.cpu().tolist()
+    ids = [(pool[i].id, pool[j].id) for i, j in dt.pairs]
+    rl, rh, fid = (x.cpu().tolist() for x in (dt.r_light, dt.r_heavy, dt.fid))
+    host_rows = [SimpleNamespace(light_id=ids[p][0], heavy_id=ids[p][1], theta=0.0, tau=0.0,
+                                 r_light=a, r_heavy=b, fidelity_cost=f)
+                 for p, a, b, f in zip(pair_ids, rl, rh, fid)]
+    t0 = time.perf_counter()
+    agree = True
+    for i in range(cpu_points):
+        k = (i * 397) % P
+        want = op.solve(host_rows, cat, lams[k], {}, cfg.workers, slos[k], 1.5)
+        agree &= want["row_index"] == int(out["row"][k].item())
+    cpu_ms = (time.perf_counter() - t0) * 1e3 / cpu_points
+    return {"workload": f"c5: {P} (lambda, T_slo) points x c2 Pareto table ({rows} rows) x "
+                        f"batch combos x worker splits of W={cfg.workers}",
+            "points": P, "rows": rows, "ms_per_sweep": ms, "points_per_s": P / (ms * 1e-3),
+            "row_evals_per_s": P * rows / (ms * 1e-3),
+            "combo_evals_per_s": P * rows * combos / (ms * 1e-3),
+            "cpu_ms_per_point": cpu_ms, "cpu_points_sampled": cpu_points,
+            "cpu_kind": "port", "cpu_agrees": bool(agree)}
 
 
 def _ncu_traffic(name):

@@ -116,6 +116,39 @@ class DeviceRows:
         self.d_lat1 = torch.from_numpy(lat1).to(dev)
         self._ws = None
 
+    @classmethod
+    def from_device_table(cls, dt, pool, catalog):
+        """Planner rows straight from a profiler DeviceTable (no host row
+        objects): light/heavy catalog indices per pair, shares and fidelity stay
+        on the device.  ``rows`` is left empty; plans carry row indices."""
+        torch = _lib.torch_cuda()
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.catalog = catalog
+        self.device = dt.pair.device
+        ids = [v.id for v in catalog.variants]
+        self.model_ids = ids
+        index = {m: i for i, m in enumerate(ids)}
+        self.batch_sizes = tuple(catalog.batch_sizes)
+        pm = torch.tensor([(index[pool[i].id], index[pool[j].id]) for i, j in dt.pairs],
+                          dtype=torch.int32, device=self.device)
+        self.d_model = pm[dt.pair.long()].contiguous()
+        self.d_share = torch.stack([dt.r_light, dt.r_heavy], dim=1).contiguous()
+        self.d_fid = dt.fid.contiguous()
+        variants = [catalog.by_id(m) for m in ids]
+        bs = self.batch_sizes
+        self.d_batch = torch.tensor(bs, dtype=torch.int32, device=self.device)
+        self.d_lat = torch.tensor([[v.latency_s[b] for b in bs] for v in variants],
+                                  dtype=torch.float64, device=self.device)
+        self.d_mu = torch.tensor([[v.throughput_qps[b] for b in bs] for v in variants],
+                                 dtype=torch.float64, device=self.device)
+        self.d_lat1 = torch.tensor([v.latency_s.get(1, float("nan")) for v in variants],
+                                   dtype=torch.float64, device=self.device)
+        self.rows = ()
+        self.n_rows = int(dt.n_rows)
+        self._ws = None
+        return self
+
     def queue_matrix(self, queues_list):
         q = np.zeros((len(queues_list), len(self.model_ids)), dtype=np.float64)
         col = {m: i for i, m in enumerate(self.model_ids)}
@@ -131,7 +164,8 @@ class DeviceRows:
         dev = self.device
         P = int(lam.shape[0])
         lib = _lib.load()
-        ws_bytes = lib.hadis_solve_workspace_bytes(P, len(self.rows))
+        n_rows = len(self.rows) if self.rows else self.n_rows
+        ws_bytes = lib.hadis_solve_workspace_bytes(P, n_rows)
         if self._ws is None or self._ws.numel() < ws_bytes:
             self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         out = dict(row=torch.empty(P, dtype=torch.int32, device=dev),
@@ -141,7 +175,7 @@ class DeviceRows:
                    flags=torch.empty(P, dtype=torch.int32, device=dev))
         p = _lib.ptr
         _lib.check(lib.hadis_solve_many(
-            len(self.rows), p(self.d_model), p(self.d_share), p(self.d_fid), len(self.model_ids),
+            n_rows, p(self.d_model), p(self.d_share), p(self.d_fid), len(self.model_ids),
             len(self.batch_sizes), p(self.d_batch), p(self.d_lat), p(self.d_mu), p(self.d_lat1), P,
             p(lam), p(t_slo), p(workers), p(qmat), float(alpha), p(out["row"]), p(out["x"]),
             p(out["b"]), p(out["path"]), p(out["flags"]), p(self._ws), ws_bytes,
