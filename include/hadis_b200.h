@@ -94,13 +94,15 @@ size_t hadis_bin_hist_sorted_workspace_bytes(int64_t n, int32_t n_unique);
 int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfix_sorted,
                           const double* scores_sorted, int64_t n, int32_t n_light,
                           const double* thr_unique, int32_t n_unique, uint32_t* hist_cnt,
-                          uint64_t* hist_hsum, void* workspace, size_t workspace_bytes,
-                          void* stream);
+                          uint64_t* hist_hsum, uint8_t* row_scanned, void* workspace,
+                          size_t workspace_bytes, void* stream);
 
 /* K2 -- in-place 2-D inclusive prefix sums of the K1 histograms:
- *   cnt[l][k][t] = #{q : bh(q) <= k, bs_l(q) <= t}  (and the same for hsum). */
+ *   cnt[l][k][t] = #{q : bh(q) <= k, bs_l(q) <= t}  (and the same for hsum).
+ * row_scanned[l][k] != 0 (may be NULL) marks rows K1 already prefix-summed
+ * along bs (hadis_bin_hist_sorted does so for every row it owns whole). */
 int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t n_light,
-                    int32_t n_unique, void* stream);
+                    int32_t n_unique, const uint8_t* row_scanned, void* stream);
 
 /* Per-pair parameters, row-major [n_pairs][HADIS_PAIR_PARAMS] doubles:
  * {latency_s[1] light, latency_s[1] heavy, base cost light, penalty light,

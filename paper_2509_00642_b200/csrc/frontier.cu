@@ -121,6 +121,7 @@ __device__ __forceinline__ void cell_numerators(const Grid& g, const PairConst& 
 struct CellInts {
   uint32_t Rk, nH;       // records kept by the light stage; heavy-served records
   uint64_t SH, SL;       // fixed-point hardness sums of heavy / light-served records
+  double dRk, dnH, dnL, dSH, dSL;   // the same, converted once for every partner
 };
 
 __device__ __forceinline__ CellInts cell_ints(const Grid& g, const uint32_t* C, const uint64_t* Sh,
@@ -132,16 +133,20 @@ __device__ __forceinline__ CellInts cell_ints(const Grid& g, const uint32_t* C, 
   c.nH = ((uint32_t)g.n - c.Rk) + C[rk + t];
   c.SH = (Htot - Sh[rk + g.U]) + Sh[rk + t];
   c.SL = Htot - c.SH;
+  c.dRk = (double)c.Rk;
+  c.dnH = (double)c.nH;
+  c.dnL = (double)((uint32_t)g.n - c.nH);
+  c.dSH = (double)c.SH;
+  c.dSL = (double)c.SL;
   return c;
 }
 
 __device__ __forceinline__ void numerators_of(const Grid& g, const PairConst& pc, const CellInts& c,
                                               double* x, double* S) {
-  *x = __dadd_rn(__dmul_rn((double)c.Rk, pc.Ll), __dmul_rn((double)c.nH, pc.Lh));
-  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)c.SH),
-                                           __dmul_rn(pc.pl, (double)c.SL)), g.inv_scale);
-  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, (double)c.nH),
-                           __dmul_rn(pc.bl, (double)((uint32_t)g.n - c.nH))), hterm);
+  *x = __dadd_rn(__dmul_rn(c.dRk, pc.Ll), __dmul_rn(c.dnH, pc.Lh));
+  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, c.dSH), __dmul_rn(pc.pl, c.dSL)),
+                                 g.inv_scale);
+  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, c.dnH), __dmul_rn(pc.bl, c.dnL)), hterm);
 }
 
 // bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
@@ -340,28 +345,52 @@ __device__ __forceinline__ unsigned long long block_exclusive_min(unsigned long 
   return before;
 }
 
-// per pair: exclusive prefix-min over bucket minima, tiles of 4 x blockDim keys
+// per pair: exclusive prefix-min over bucket minima, in three grid-wide phases
+// (tile minima -> per-pair scan of tile minima -> in-tile scan with carry)
+constexpr int kPrefTile = 4 * kScanThreads;
+
 __global__ void __launch_bounds__(kScanThreads)
-bucket_prefix_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
-                     double* __restrict__ gpre) {
-  const int p = blockIdx.x;
+prefix_tile_min_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
+                       unsigned long long* __restrict__ tmin) {
+  const int p = blockIdx.y, tile = blockIdx.x;
+  const int i0 = tile * kPrefTile + 4 * threadIdx.x;
+  const unsigned long long* src = bmin + (int64_t)p * nbuckets;
+  unsigned long long m = ~0ull;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) if (i0 + j < nbuckets) m = min(m, src[i0 + j]);
+  unsigned long long total;
+  block_exclusive_min(m, &total);
+  if (threadIdx.x == 0) tmin[(int64_t)p * gridDim.x + tile] = total;
+}
+
+__global__ void prefix_carry_kernel(unsigned long long* __restrict__ tmin, int tiles, int n_pairs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  unsigned long long run = ~0ull;
+  for (int t = 0; t < tiles; ++t) {
+    const unsigned long long v = tmin[(int64_t)p * tiles + t];
+    tmin[(int64_t)p * tiles + t] = run;          // exclusive
+    run = min(run, v);
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+prefix_apply_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
+                    const unsigned long long* __restrict__ tcarry, double* __restrict__ gpre) {
+  const int p = blockIdx.y, tile = blockIdx.x;
+  const int i0 = tile * kPrefTile + 4 * threadIdx.x;
   const unsigned long long* src = bmin + (int64_t)p * nbuckets;
   double* dst = gpre + (int64_t)p * nbuckets;
-  unsigned long long carry = ~0ull;
-  for (int base = 0; base < nbuckets; base += 4 * blockDim.x) {
-    const int i0 = base + 4 * threadIdx.x;
-    unsigned long long v[4];
-    unsigned long long m = ~0ull;
+  unsigned long long v[4];
+  unsigned long long m = ~0ull;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { v[j] = i0 + j < nbuckets ? src[i0 + j] : ~0ull; m = min(m, v[j]); }
-    unsigned long long total;
-    unsigned long long run = min(carry, block_exclusive_min(m, &total));
+  for (int j = 0; j < 4; ++j) { v[j] = i0 + j < nbuckets ? src[i0 + j] : ~0ull; m = min(m, v[j]); }
+  unsigned long long total;
+  unsigned long long run = min(tcarry[(int64_t)p * gridDim.x + tile], block_exclusive_min(m, &total));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (i0 + j < nbuckets) dst[i0 + j] = run == ~0ull ? INFINITY : from_order_key(run);
-      run = min(run, v[j]);
-    }
-    carry = min(carry, total);
+  for (int j = 0; j < 4; ++j) {
+    if (i0 + j < nbuckets) dst[i0 + j] = run == ~0ull ? INFINITY : from_order_key(run);
+    run = min(run, v[j]);
   }
 }
 
@@ -374,54 +403,6 @@ struct Cands {
   double* lat;
   double* fid;
 };
-
-// Two passes over the cells: COUNT candidates per (pair, bucket), scan the
-// counts into bucket offsets, then WRITE every candidate straight into its
-// bucket's segment -- no global candidate counter, no separate scatter.
-template <bool kWrite>
-__global__ void __launch_bounds__(kCellThreads)
-filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
-              const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
-              uint32_t* __restrict__ bcnt, const unsigned long long* __restrict__ boff,
-              uint32_t* __restrict__ bcur, Cands grp, int64_t cap) {
-  const int gi = blockIdx.y;
-  if (gi >= *n_groups) return;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)g.U * g.U) return;
-  const int k = (int)(c / g.U), t = (int)(c % g.U);
-  const int p0 = group_p0[gi], p1 = group_p0[gi + 1];
-  const int slot = pcs[p0].slot;
-  const uint32_t* C = slot_cnt(g, slot);
-  if (!class_start(g, C, k, t)) return;
-  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
-  const double dn = (double)g.n;
-  uint32_t rep = 0xffffffffu;
-  for (int p = p0; p < p1; ++p) {
-    const PairConst pc = pcs[p];
-    double x, S;
-    numerators_of(g, pc, ci, &x, &S);
-    const int b = bucket_of_x(pc, g.nbuckets, x);
-    const int64_t key = (int64_t)p * g.nbuckets + b;
-    if (!(S <= gpre[key] + pc.delta2_S)) continue;
-    if (!kWrite) {
-      atomicAdd(&bcnt[key], 1u);
-      continue;
-    }
-    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
-    if (at >= cap) continue;
-    if (rep == 0xffffffffu) rep = rep_cell(g, C, k, t, true);
-    grp.pair[at] = (uint32_t)p;
-    grp.cell[at] = rep;
-    grp.bucket[at] = (uint32_t)b;
-    grp.lat[at] = __ddiv_rn(x, dn);
-    grp.fid[at] = __ddiv_rn(S, dn);
-  }
-}
-
-__global__ void candidates_total_kernel(const unsigned long long* __restrict__ total,
-                                        unsigned long long* __restrict__ counters) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = *total;
-}
 
 // ---------------------------------------------- F4: offsets (exclusive scan)
 
@@ -539,75 +520,138 @@ __device__ __forceinline__ bool kills(double fd, double fc, double lat_d, double
   return fd < fc || (fd == fc && (lat_d < lat_c || idx_d < idx_c));
 }
 
+struct DecideOut {
+  uint32_t* kept_bm;
+  Uncertain un;
+  int64_t ucap;
+  uint32_t* req_bm;
+  uint32_t* req_pair;
+  uint32_t* req_cell;
+  int64_t rcap;
+  unsigned long long* counters;
+};
+
+// Certified main-universe decision for candidate `self` (pair p, representative
+// cell, bucket-mates grp[s0, s1)); G_S = exclusive prefix-min numerator of its
+// bucket.  Keeps, drops or queues the cell for the exact-fidelity resolution.
+__device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t cell, double lat,
+                           double fid, double G_S, const Cands& grp, int64_t s0, int64_t s1,
+                           int64_t self, const DecideOut& o) {
+  const int k = (int)(cell / g.U), t = (int)(cell % g.U);
+  const int64_t idx = grid_index(g, k, t);
+  bool killed = false, unsure = false;
+  // fl(S / n) is exactly the lower buckets' min fid*
+  const double G = __ddiv_rn(G_S, (double)g.n);
+  if (G < fid - pc.delta2) {
+    killed = true;
+  } else if (G <= fid + pc.delta2) {
+    // a lower-bucket cell is close: certain only if it is this cell's
+    // heavy-set twin with more bypass (equal fidelity, strictly lower latency)
+    unsure = true;
+    const int kp = g.pk[k];
+    if (kp >= 0) {
+      const uint32_t* C = slot_cnt(g, pc.slot);
+      const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
+      if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
+        const CellVal tw = eval_cell(g, pc, kp, t);
+        if (tw.lat < lat) {
+          killed = true;
+        } else if (tw.lat == lat) {
+          const uint32_t tc = rep_cell(g, C, kp, t);
+          if (grid_index(g, (int)(tc / g.U), (int)(tc % g.U)) < idx) killed = true;
+        }
+      }
+    }
+  }
+  for (int64_t j = s0; j < s1 && !killed; ++j) {
+    if (j == self) continue;
+    const double ld = grp.lat[j];
+    if (ld > lat) continue;
+    const double fd = grp.fid[j];
+    const uint32_t dc = grp.cell[j];
+    const int kd = (int)(dc / g.U), td = (int)(dc % g.U);
+    if (fabs(fd - fid) > pc.delta2) {
+      if (fd < fid) killed = true;
+    } else if (same_heavy(g, pc.slot, kd, td, k, t)) {
+      if (ld < lat || grid_index(g, kd, td) < idx) killed = true;
+    } else {
+      unsure = true;
+    }
+  }
+  if (killed) return;
+  const int64_t cells = (int64_t)g.U * g.U;
+  if (!unsure) {
+    set_bit(o.kept_bm, (int64_t)p * g.bm_stride + cell);
+  } else {
+    push_uncertain(0, p, cell, o.un, o.ucap, o.counters);
+    request_exact(cells, p, cell, o.req_bm, o.req_pair, o.req_cell, o.rcap, o.counters);
+  }
+}
+
+// Two passes over the cells: COUNT candidates per (pair, bucket), scan the
+// counts into bucket offsets, then WRITE every candidate straight into its
+// bucket's segment -- no global candidate counter, no separate scatter.
+template <bool kWrite>
+__global__ void __launch_bounds__(kCellThreads)
+filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
+              const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
+              uint32_t* __restrict__ bcnt, const unsigned long long* __restrict__ boff,
+              uint32_t* __restrict__ bcur, Cands grp, int64_t cap, DecideOut o) {
+  const int gi = blockIdx.y;
+  if (gi >= *n_groups) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)g.U * g.U) return;
+  const int k = (int)(c / g.U), t = (int)(c % g.U);
+  const int p0 = group_p0[gi], p1 = group_p0[gi + 1];
+  const int slot = pcs[p0].slot;
+  const uint32_t* C = slot_cnt(g, slot);
+  if (!class_start(g, C, k, t)) return;
+  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
+  const double dn = (double)g.n;
+  uint32_t rep = 0xffffffffu;
+  for (int p = p0; p < p1; ++p) {
+    const PairConst pc = pcs[p];
+    double x, S;
+    numerators_of(g, pc, ci, &x, &S);
+    const int b = bucket_of_x(pc, g.nbuckets, x);
+    const int64_t key = (int64_t)p * g.nbuckets + b;
+    if (!(S <= gpre[key] + pc.delta2_S)) continue;
+    if (!kWrite) {
+      atomicAdd(&bcnt[key], 1u);
+      continue;
+    }
+    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
+    if (at >= cap) continue;
+    if (rep == 0xffffffffu) rep = rep_cell(g, C, k, t, true);
+    const double lat = __ddiv_rn(x, dn), fid = __ddiv_rn(S, dn);
+    grp.pair[at] = (uint32_t)p;
+    grp.cell[at] = rep;
+    grp.bucket[at] = (uint32_t)b;
+    grp.lat[at] = lat;
+    grp.fid[at] = fid;
+  }
+}
+
+__global__ void candidates_total_kernel(const unsigned long long* __restrict__ total,
+                                        unsigned long long* __restrict__ counters) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = *total;
+}
+
+// one thread per candidate; bucket-mates are the candidates of its segment
 __global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
                               const unsigned long long* __restrict__ counters_ro, int64_t cap,
                               const unsigned long long* __restrict__ boff,
                               const uint32_t* __restrict__ bcnt, const double* __restrict__ gpre,
-                              Cands grp, uint32_t* kept_bm,
-                              Uncertain un, int64_t ucap, uint32_t* req_bm, uint32_t* req_pair,
-                              uint32_t* req_cell, int64_t rcap, unsigned long long* counters) {
+                              Cands grp, DecideOut o) {
   if ((int64_t)counters_ro[0] > cap) return;
   const int64_t m = (int64_t)counters_ro[0];
-  const int64_t cells = (int64_t)g.U * g.U;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     const int p = (int)grp.pair[i];
-    const uint32_t cell = grp.cell[i];
-    const int k = (int)(cell / g.U), t = (int)(cell % g.U);
-    const int b = (int)grp.bucket[i];
-    const double lat = grp.lat[i], fid = grp.fid[i];
-    const PairConst pc = pcs[p];
-    const int64_t idx = grid_index(g, k, t);
-    bool killed = false, unsure = false;
-    // gpre holds numerators S; fl(S / n) is exactly the lower buckets' min fid*
-    const double G = __ddiv_rn(gpre[(int64_t)p * g.nbuckets + b], (double)g.n);
-    if (G < fid - pc.delta2) {
-      killed = true;
-    } else if (G <= fid + pc.delta2) {
-      // a lower-bucket cell is close: certain only if it is c's heavy-set twin
-      // with more bypass (equal fidelity, strictly lower latency)
-      unsure = true;
-      const int kp = g.pk[k];
-      if (kp >= 0) {
-        const uint32_t* C = slot_cnt(g, pc.slot);
-        const int64_t rk = (int64_t)k * g.B1, rp = (int64_t)kp * g.B1;
-        if (C[rk + t] - C[rp + t] == C[rk + g.U] - C[rp + g.U]) {
-          const CellVal tw = eval_cell(g, pc, kp, t);
-          if (tw.lat < lat) {
-            killed = true;
-          } else if (tw.lat == lat) {
-            const uint32_t tc = rep_cell(g, C, kp, t);
-            if (grid_index(g, (int)(tc / g.U), (int)(tc % g.U)) < idx) killed = true;
-          }
-        }
-      }
-    }
-    if (!killed) {
-      const int64_t key = (int64_t)p * g.nbuckets + b;
-      const int64_t s0 = (int64_t)boff[key], s1 = s0 + bcnt[key];
-      for (int64_t j = s0; j < s1 && j < m; ++j) {
-        if (j == i) continue;
-        const double ld = grp.lat[j];
-        if (ld > lat) continue;
-        const double fd = grp.fid[j];
-        const uint32_t dc = grp.cell[j];
-        const int kd = (int)(dc / g.U), td = (int)(dc % g.U);
-        if (fabs(fd - fid) > pc.delta2) {
-          if (fd < fid) { killed = true; break; }
-        } else if (same_heavy(g, pc.slot, kd, td, k, t)) {
-          if (ld < lat || grid_index(g, kd, td) < idx) { killed = true; break; }
-        } else {
-          unsure = true;
-        }
-      }
-    }
-    if (killed) continue;
-    if (!unsure) {
-      set_bit(kept_bm, (int64_t)p * g.bm_stride + cell);
-    } else {
-      push_uncertain(0, p, cell, un, ucap, counters);
-      request_exact(cells, p, cell, req_bm, req_pair, req_cell, rcap, counters);
-    }
+    const int64_t key = (int64_t)p * g.nbuckets + grp.bucket[i];
+    const int64_t s0 = (int64_t)boff[key];
+    decide_one(g, pcs[p], p, grp.cell[i], grp.lat[i], grp.fid[i], gpre[key], grp, s0,
+               min(s0 + (int64_t)bcnt[key], m), i, o);
   }
 }
 
@@ -1044,7 +1088,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 
 struct Layout {
   size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, grp[5], kept, reqbm, un[3], req[3],
-      counters, groups, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
+      counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1076,6 +1120,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.req[0] = take(4 * ecap); L.req[1] = take(4 * ecap); L.req[2] = take(8 * ecap);
   L.counters = take(8 * 8);
   L.groups = take(4 * (n_pairs + 2));
+  L.tmin = take(8 * (ceil_div(nbuckets, 4096) * n_pairs + 1));
   L.pwplan = take(sizeof(PwPlan));
   const int64_t pw_batch = std::min<int64_t>(std::max(ecap, out_cap), kPwCellsPerLaunch);
   L.pwvals = take(8 * (int64_t)kPwPlanNodes * pw_batch);
@@ -1153,6 +1198,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   unsigned long long* counters = (unsigned long long*)P(L.counters);
   int32_t* n_groups = (int32_t*)P(L.groups);
   int32_t* group_p0 = n_groups + 1;
+  unsigned long long* tmin = (unsigned long long*)P(L.tmin);
   PwPlan* pwplan = (PwPlan*)P(L.pwplan);
   double* pwvals = (double*)P(L.pwvals);
   uint32_t* chunk_rows = (uint32_t*)P(L.pair_rows);
@@ -1173,7 +1219,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
-  int launches = 26;   // fixed kernels below; batched emulation adds 2 per batch
+  int launches = 28;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
@@ -1187,9 +1233,15 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   const dim3 cell_grid((unsigned)ceil_div(cells, kCellThreads), (unsigned)n_pairs);
   group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups);
   bucket_min_kernel<<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, bmin);
-  bucket_prefix_kernel<<<n_pairs, kScanThreads, 0, st>>>(bmin, nb, gpre);
+  {
+    const int tiles = (int)ceil_div(nb, kPrefTile);
+    prefix_tile_min_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin);
+    prefix_carry_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(tmin, tiles, n_pairs);
+    prefix_apply_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin, gpre);
+  }
+  const DecideOut dout{kept, un, exact_cap, reqbm, req_pair, req_cell, exact_cap, counters};
   filter_kernel<false><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
-                                                          boff, bcur, grp, cand_cap);
+                                                          boff, bcur, grp, cand_cap, dout);
   {
     const int64_t tiles = ceil_div(pb, kScanTile);
     tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum);
@@ -1198,11 +1250,10 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
   filter_kernel<true><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
-                                                         boff, bcur, grp, cand_cap);
+                                                         boff, bcur, grp, cand_cap, dout);
   HADIS_LAUNCH_CHECK();
-  decide_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
-                                             grp, kept, un, exact_cap, reqbm, req_pair, req_cell,
-                                             exact_cap, counters);
+  decide_kernel<<<kNumSMs * 8, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
+                                             grp, dout);
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
   if (row_smem > 48 * 1024)
     HADIS_CUDA_TRY(cudaFuncSetAttribute(nobypass_kernel,

@@ -93,10 +93,10 @@ bin_hist_global_kernel(const double* __restrict__ h, const double* __restrict__ 
 
 // K2a: inclusive prefix along bs (the contiguous axis): one warp per row.
 __global__ void scan_rows_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs,
-                                 int64_t rows, int B1) {
+                                 int64_t rows, int B1, const uint8_t* __restrict__ done) {
   const int lane = threadIdx.x & 31;
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= rows) return;
+  if (row >= rows || (done && done[row])) return;
   uint32_t* c = cnt + row * B1;
   unsigned long long* s = hs + row * B1;
   uint32_t carry_c = 0;
@@ -206,13 +206,13 @@ extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, 
 }
 
 extern "C" int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t n_light,
-                               int32_t n_unique, void* stream) {
+                               int32_t n_unique, const uint8_t* row_scanned, void* stream) {
   if (!hist_cnt || !hist_hsum || n_light <= 0 || n_unique <= 0) return HADIS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const int B1 = n_unique + 1;
   const int64_t rows = (int64_t)n_light * B1;
   scan_rows_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(
-      hist_cnt, (unsigned long long*)hist_hsum, rows, B1);
+      hist_cnt, (unsigned long long*)hist_hsum, rows, B1, row_scanned);
   HADIS_LAUNCH_CHECK();
   const int64_t cols = (int64_t)n_light * B1;
   scan_cols_kernel<<<(unsigned)ceil_div(cols, 128), 128, 0, st>>>(

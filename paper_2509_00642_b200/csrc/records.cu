@@ -148,7 +148,7 @@ row_hist_kernel(const unsigned long long* __restrict__ hf, const double* __restr
                 const double* __restrict__ thr, int U, const uint32_t* __restrict__ g_guide,
                 const int64_t* __restrict__ rb, const int64_t* __restrict__ item_off,
                 const uint8_t* __restrict__ item_narrow, uint32_t* __restrict__ g_cnt,
-                unsigned long long* __restrict__ g_hsum) {
+                unsigned long long* __restrict__ g_hsum, uint8_t* __restrict__ row_scanned) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B1 = U + 1;
   uint32_t* s_bin = reinterpret_cast<uint32_t*>(smem);          // [4][kBinStride]
@@ -199,20 +199,67 @@ row_hist_kernel(const unsigned long long* __restrict__ hf, const double* __restr
   __syncthreads();
   uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
   unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
-  for (int i = threadIdx.x; i < B1; i += blockDim.x) {
-    const uint32_t c = s_bin[i];
-    const unsigned long long v = (unsigned long long)c * base +
-                                 (unsigned long long)s_bin[kBinStride + i] +
-                                 ((unsigned long long)s_bin[2 * kBinStride + i] << 16) +
-                                 ((unsigned long long)s_bin[3 * kBinStride + i] << 32);
-    if (whole_row) {
-      gc[i] = c;
-      gh[i] = v;
-    } else if (c) {
-      atomicAdd(&gc[i], c);
-      atomicAdd(&gh[i], v);
+  auto bin_sum = [&](int i) {
+    return (unsigned long long)s_bin[i] * base + (unsigned long long)s_bin[kBinStride + i] +
+           ((unsigned long long)s_bin[2 * kBinStride + i] << 16) +
+           ((unsigned long long)s_bin[3 * kBinStride + i] << 32);
+  };
+  if (!whole_row || !row_scanned) {
+    for (int i = threadIdx.x; i < B1; i += blockDim.x) {
+      const uint32_t c = s_bin[i];
+      const unsigned long long v = bin_sum(i);
+      if (whole_row) {
+        gc[i] = c;
+        gh[i] = v;
+      } else if (c) {
+        atomicAdd(&gc[i], c);
+        atomicAdd(&gh[i], v);
+      }
     }
+    return;
   }
+  // whole row: emit the K2 row prefix (along bs) directly -- thread-contiguous
+  // segments, block scan of the segment totals, then the segment prefixes
+  __shared__ uint32_t ws_c[kK1Threads / 32];
+  __shared__ unsigned long long ws_h[kK1Threads / 32];
+  const int per = (B1 + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+  uint32_t tc = 0;
+  unsigned long long th = 0;
+  for (int i = i0; i < i1; ++i) { tc += s_bin[i]; th += bin_sum(i); }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t ic = tc;
+  unsigned long long ih = th;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, off);
+    const unsigned long long oh = __shfl_up_sync(0xffffffffu, ih, off);
+    if (lane >= off) { ic += oc; ih += oh; }
+  }
+  if (lane == 31) { ws_c[warp] = ic; ws_h[warp] = ih; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t wc = lane < nw ? ws_c[lane] : 0u;
+    unsigned long long wh = lane < nw ? ws_h[lane] : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t oc = __shfl_up_sync(0xffffffffu, wc, off);
+      const unsigned long long oh = __shfl_up_sync(0xffffffffu, wh, off);
+      if (lane >= off) { wc += oc; wh += oh; }
+    }
+    if (lane < nw) { ws_c[lane] = wc; ws_h[lane] = wh; }
+  }
+  __syncthreads();
+  uint32_t rc = (warp > 0 ? ws_c[warp - 1] : 0u) + ic - tc;
+  unsigned long long rh = (warp > 0 ? ws_h[warp - 1] : 0ull) + ih - th;
+  for (int i = i0; i < i1; ++i) {
+    rc += s_bin[i];
+    rh += bin_sum(i);
+    gc[i] = rc;
+    gh[i] = rh;
+  }
+  if (threadIdx.x == 0) row_scanned[(int64_t)l * B1 + k] = 1;
 }
 
 // per item: does its hardness span fit 32 bits (narrow) ?
@@ -276,8 +323,8 @@ extern "C" size_t hadis_bin_hist_sorted_workspace_bytes(int64_t n, int32_t n_uni
 extern "C" int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfix_sorted,
                                      const double* scores_sorted, int64_t n, int32_t n_light,
                                      const double* thr_unique, int32_t n_unique,
-                                     uint32_t* hist_cnt, uint64_t* hist_hsum, void* workspace,
-                                     size_t workspace_bytes, void* stream) {
+                                     uint32_t* hist_cnt, uint64_t* hist_hsum, uint8_t* row_scanned,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
   if (!h_sorted || !hfix_sorted || !scores_sorted || n <= 0 || n > 0xffffffffll || n_light <= 0 ||
       n_unique <= 0 || !thr_unique || !hist_cnt || !hist_hsum || !workspace || n_light > 65535)
     return HADIS_ERR_ARG;
@@ -295,6 +342,7 @@ extern "C" int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfi
   if (max_items > 65535) return HADIS_ERR_UNSUPPORTED;
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
+  if (row_scanned) HADIS_CUDA_TRY(cudaMemsetAsync(row_scanned, 0, (size_t)B1 * n_light, st));
   row_plan_kernel<<<1, 1024, 0, st>>>(h_sorted, n, thr_unique, n_unique, rb, item_off, guide);
   item_span_kernel<<<(unsigned)ceil_div(max_items, 256), 256, 0, st>>>(
       (const unsigned long long*)hfix_sorted, n_unique, rb, item_off, max_items, item_narrow);
@@ -308,10 +356,10 @@ extern "C" int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfi
   const dim3 grid((unsigned)n_light, (unsigned)max_items);
   row_hist_kernel<true><<<grid, kK1Threads, smem, st>>>(
       (const unsigned long long*)hfix_sorted, scores_sorted, n, thr_unique, n_unique, guide, rb,
-      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum);
+      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum, row_scanned);
   row_hist_kernel<false><<<grid, kK1Threads, smem, st>>>(
       (const unsigned long long*)hfix_sorted, scores_sorted, n, thr_unique, n_unique, guide, rb,
-      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum);
+      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum, row_scanned);
   HADIS_LAUNCH_CHECK();
   hadis_count_launches(4);
   return HADIS_OK;

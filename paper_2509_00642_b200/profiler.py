@@ -330,6 +330,8 @@ class GridProfiler:
         st = _lib.stream_handle(stream)
         bins = (plan.U + 1) * (plan.U + 1) * plan.n_light
         state = dict(plan=plan, exact_fid=exact_fid, stream=stream,
+                     scanned=torch.empty((plan.U + 1) * plan.n_light, dtype=torch.uint8,
+                                         device=dev),
                      cnt=torch.empty(bins, dtype=torch.int32, device=dev),
                      hsum=torch.empty(bins, dtype=torch.int64, device=dev),
                      scores=self.scores[plan.slot0:plan.slot0 + plan.n_light])
@@ -340,15 +342,17 @@ class GridProfiler:
             ss = self.ss[plan.slot0:plan.slot0 + plan.n_light]
             _lib.check(self.lib.hadis_bin_hist_sorted(
                 p(self.hs), p(self.hfs), p(ss), self.n, plan.n_light, p(plan.d_u), plan.U,
-                p(state["cnt"]), p(state["hsum"]), p(self._k1_ws), self._k1_ws.numel(), st),
-                "hadis_bin_hist_sorted")
+                p(state["cnt"]), p(state["hsum"]), p(state["scanned"]), p(self._k1_ws),
+                self._k1_ws.numel(), st), "hadis_bin_hist_sorted")
+            scanned = state["scanned"]
         else:
             _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
                                                p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
                                                p(state["hsum"]), p(self.bad), st), "hadis_bin_hist")
+            scanned = None
         rec(1)
         _lib.check(self.lib.hadis_hist_scan(p(state["cnt"]), p(state["hsum"]), plan.n_light,
-                                            plan.U, st), "hadis_hist_scan")
+                                            plan.U, p(scanned), st), "hadis_hist_scan")
         rec(2)
         self._frontier(state, plan.caps)
         rec(3)
