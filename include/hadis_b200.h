@@ -57,19 +57,9 @@ int64_t hadis_kernel_launches(void);
 
 /* Fixed-point scale for hardness sums: h_fix = floor(h * 2^shift), with
  * shift = min(48, 63 - bit_length(n)) so every sum of n values fits in 63 bits
- * and one record's h_fix splits into three 16-bit K1 shared-memory limbs. */
+ * and one record's h_fix (relative to its row's lower bound) splits into at most
+ * three 16-bit K1 shared-memory limbs. */
 int hadis_hfix_shift(int64_t n);
-
-/* Record-store ingest: order records by hardness (ties by original index) and
- * gather the n_rows score rows (row stride n) into the same order; hfix_sorted
- * receives floor(h * 2^hfix_shift) of each sorted record.  perm (may be NULL)
- * receives the original index of each sorted position; bad_records counts
- * hardness values that are NaN or outside [0, 1]. */
-size_t hadis_records_workspace_bytes(int64_t n);
-int hadis_records_sort(const double* h, const double* scores, int64_t n, int32_t n_rows,
-                       int32_t hfix_shift, double* h_sorted, uint64_t* hfix_sorted,
-                       double* scores_sorted, uint32_t* perm, uint32_t* bad_records,
-                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* K1 -- bin + 2-D histogram (profiler.py:138, 145-150: bypass h > theta,
  * reject score < tau), records in any order.  For every record q and light
@@ -85,17 +75,31 @@ int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_l
                    uint32_t* hist_cnt, uint64_t* hist_hsum, uint32_t* bad_records,
                    void* stream);
 
-/* K1 on a hardness-sorted record store (profiler.py:138, 145-150): same
- * histogram as hadis_bin_hist, built without global atomics -- each row of
- * equal bh is a contiguous run of sorted records, so one CTA per (row chunk,
- * light model) accumulates in shared memory and stores the row.  Supports up
- * to 2047 distinct thresholds (hadis_bin_hist covers larger grids). */
-size_t hadis_bin_hist_sorted_workspace_bytes(int64_t n, int32_t n_unique);
-int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfix_sorted,
-                          const double* scores_sorted, int64_t n, int32_t n_light,
-                          const double* thr_unique, int32_t n_unique, uint32_t* hist_cnt,
-                          uint64_t* hist_hsum, uint8_t* row_scanned, void* workspace,
-                          size_t workspace_bytes, void* stream);
+/* Row-bucketed record store (profiler.py:138, 145-150), per threshold grid:
+ * records are grouped by their theta-row bh = #{u < h} so that K1 needs no
+ * global atomics.  One pass reads h and the n_light score rows (row stride n)
+ * once and writes, row-bucketed (rows in bh order, order within a row
+ * unspecified):
+ *   hfix_rows[i]       = floor(h * 2^hfix_shift)          (uint64[n])
+ *   bs_rows[l][i]      = #{u <= s_l}  (the tau-bin)        (uint16[n_light][n])
+ * row_plan (hadis_row_plan_bytes) receives the row offsets and K1's work
+ * items; pass it unchanged to hadis_bin_hist_rows.  bad_records (device
+ * uint32, may be NULL) counts hardness values that are NaN or outside [0, 1].
+ * Supports up to 2047 distinct thresholds (hadis_bin_hist covers larger). */
+size_t hadis_row_plan_bytes(int32_t n_unique);
+int hadis_records_bucket(const double* h, const double* scores, int64_t n, int32_t n_light,
+                         const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
+                         uint64_t* hfix_rows, uint16_t* bs_rows, uint32_t* bad_records,
+                         void* row_plan, size_t row_plan_bytes, void* stream);
+
+/* K1 on the row-bucketed store: the same histogram as hadis_bin_hist, one CTA
+ * per (row chunk, light model) accumulating in shared memory.  Rows a CTA
+ * owns whole are stored already prefix-summed along bs and flagged in
+ * row_scanned[l][k] (may be NULL: plain histogram). */
+int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs_rows, int64_t n,
+                        int32_t n_light, int32_t n_unique, const void* row_plan,
+                        uint32_t* hist_cnt, uint64_t* hist_hsum, uint8_t* row_scanned,
+                        void* stream);
 
 /* K2 -- in-place 2-D inclusive prefix sums of the K1 histograms:
  *   cnt[l][k][t] = #{q : bh(q) <= k, bs_l(q) <= t}  (and the same for hsum).

@@ -33,12 +33,11 @@ _SIGNATURES = {
     "hadis_bin_hist": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp,
                                 _c_vp, _c_vp]),
     "hadis_hist_scan": (_c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
-    "hadis_records_workspace_bytes": (_c_sz, [_c_i64]),
-    "hadis_records_sort": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp,
-                                    _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
-    "hadis_bin_hist_sorted_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
-    "hadis_bin_hist_sorted": (_c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_vp,
-                                       _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "hadis_row_plan_bytes": (_c_sz, [_c_i32]),
+    "hadis_records_bucket": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
+                                      _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "hadis_bin_hist_rows": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp,
+                                     _c_vp, _c_vp]),
     "hadis_frontier_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i64, _c_i64, _c_i64]),
     "hadis_pair_frontiers": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_vp, _c_vp,
                                       _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_i32, _c_vp, _c_sz,

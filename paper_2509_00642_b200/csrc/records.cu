@@ -1,208 +1,407 @@
-// Record store layout + K1 (bin + 2-D histogram) from hardness-sorted records.
+// Row-bucketed record store + K1 (2-D histogram), per threshold grid.
 //
-// Ingest (once per record set, hadis_records_sort): records are ordered by
-// hardness (ties by original index, so the layout is deterministic) and the
-// score rows are gathered into the same order.  The original-order arrays
-// stay with the caller for the numpy-exact fidelity emulation.
+// Reference semantics (pkg/src/cascadesim/profiler.py:138, 145-150):
+//   bypass(q, theta) = h[q] > theta,  reject(q, tau) = not bypass and s[q] < tau
+// With u = the sorted distinct thresholds (U values):
+//   bh(q) = #{u < h[q]}   (the theta-row of record q)
+//   bs(q) = #{u <= s[q]}  (its tau-bin for one light model)
 //
-// Then, for ANY threshold grid, bh(q) = #{u < h[q]} is constant on a
-// contiguous run of sorted records (a "row"), so K1 needs no global atomics:
-// one CTA owns (row k, light model l, record range) and accumulates the row's
-// bs-histogram (counts + fixed-point hardness) in shared memory with 32-bit
-// ATOMS, then writes it out -- plain stores when it owns the whole row.
-// Bins are (count, three 16-bit hardness limbs) with hardness in <= 48-bit
-// fixed point; a CTA sees at most kRowChunk records, so no limb can overflow.
+// B0 setup    guide tables (h: #{u < x}, s: #{u <= x}) over [0, 1] in 4096
+//             buckets, zeroed row counters.
+// B1 count    records -> bh, CTA-private shared-memory row histogram, one
+//             global atomic per non-empty row per CTA.  Validates h in [0, 1].
+// B2 plan     row offsets (exclusive scan), per-row write cursors, K1 items
+//             (row chunks of <= kRowChunk records), per-row fixed-point bounds.
+// B3 scatter  the HBM-bound pass: every record array is read once (128-bit
+//             loads); per tile, records are counting-sorted by bh in shared
+//             memory (ATOMS ranks + one global cursor reservation per row),
+//             then written row-bucketed and staged so consecutive threads
+//             store consecutive addresses: hfix = floor(h * 2^shift) as u64
+//             and, per light model, the tau-bin bs as u16 (the score itself
+//             is never needed again).  Order within a row is irrelevant:
+//             every K1 sum is an integer sum.
+// K1 row_hist one CTA per (row chunk, light model) accumulates the row's
+//             bs-histogram (count + 16-bit hardness limbs relative to the
+//             row's fixed-point lower bound) with shared-memory ATOMS and
+//             stores the row, already prefix-summed along bs when it owns
+//             the whole row (K2's row pass fused).
+// The original-order arrays stay with the caller for the numpy-exact
+// fidelity emulation, which depends on the reference's summation order.
 #include <cmath>
 
 #include "common.cuh"
 
 namespace hadis {
 
+constexpr int kGuide = 4096;          // guide buckets over [0, 1]
+constexpr int kMaxBins = 2048;        // U + 1 <= kMaxBins (u16 bins)
+constexpr int kRowChunk = 32768;      // records per K1 CTA: 2^15 * 2^16 < 2^31 per limb
 constexpr int kK1Threads = 512;
-constexpr int kRowChunk = 32768;      // records per CTA: 32768 * 2^16 = 2^31 per limb
-constexpr int kGuide = 4096;          // score guide table buckets over [0, 1]
+constexpr int kBkThreads = 512;       // scatter CTA
+constexpr int kBkTile = 4096;         // records per scatter tile
+constexpr int kBkPer = kBkTile / kBkThreads;   // records per thread per tile (even)
+constexpr int kCountThreads = 512;
 
-__global__ void gather_kernel(const double* __restrict__ h, const double* __restrict__ scores,
-                              int64_t n, int n_rows, const uint32_t* __restrict__ idx,
-                              double hscale, double* __restrict__ h_sorted,
-                              unsigned long long* __restrict__ hfix_sorted,
-                              double* __restrict__ s_sorted, uint32_t* __restrict__ perm,
-                              uint32_t* __restrict__ bad) {
-  uint32_t my_bad = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t q = idx[i];
-    const double hq = h[q];
-    const bool ok = hq >= 0.0 && hq <= 1.0;
-    my_bad += !ok;
-    h_sorted[i] = hq;
-    hfix_sorted[i] = (unsigned long long)__dmul_rn(ok ? hq : 0.0, hscale);
-    if (perm) perm[i] = q;
-    int l = 0;
-    for (; l + 8 <= n_rows; l += 8) {      // 8 random gathers in flight per thread
-      double v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = scores[(int64_t)(l + j) * n + q];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) s_sorted[(int64_t)(l + j) * n + i] = v[j];
-    }
-    for (; l < n_rows; ++l) s_sorted[(int64_t)l * n + i] = scores[(int64_t)l * n + q];
-  }
-  if (my_bad) atomicAdd(bad, my_bad);
+// Row plan (the `row_plan` buffer shared by B0..B3 and K1), offsets in bytes.
+struct RowPlan {
+  uint32_t* row_cnt;     // [kMaxBins]     B1 counts
+  uint32_t* cursor;      // [kMaxBins]     B3 write cursors
+  int64_t* row_off;      // [kMaxBins + 1] row start offsets (row_off[U+1] = n)
+  int64_t* item_off;     // [kMaxBins + 1] first K1 item of each row
+  uint64_t* row_base;    // [kMaxBins]     fixed-point lower bound of the row's hfix
+  uint8_t* row_narrow;   // [kMaxBins]     hfix span of the row < 2^32
+  uint32_t* guide_lt;    // [kGuide + 1]
+  uint32_t* guide_le;    // [kGuide + 1]
+  uint32_t* bad;         // [1]
+};
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline RowPlan row_plan_at(void* base) {
+  unsigned char* p = (unsigned char*)base;
+  RowPlan r;
+  size_t o = 0;
+  r.row_cnt = (uint32_t*)(p + o);     o += align256(4 * kMaxBins);
+  r.cursor = (uint32_t*)(p + o);      o += align256(4 * kMaxBins);
+  r.row_off = (int64_t*)(p + o);      o += align256(8 * (kMaxBins + 1));
+  r.item_off = (int64_t*)(p + o);     o += align256(8 * (kMaxBins + 1));
+  r.row_base = (uint64_t*)(p + o);    o += align256(8 * kMaxBins);
+  r.row_narrow = (uint8_t*)(p + o);   o += align256(kMaxBins);
+  r.guide_lt = (uint32_t*)(p + o);    o += align256(4 * (kGuide + 1));
+  r.guide_le = (uint32_t*)(p + o);    o += align256(4 * (kGuide + 1));
+  r.bad = (uint32_t*)(p + o);         o += align256(4);
+  return r;
 }
 
-// row boundaries: rb[k] = #{h <= u[k-1]} (rb[0] = 0, rb[U+1] = n); rows with
-// more than kRowChunk records are split into chunks; item_off = prefix of chunks
-__global__ void __launch_bounds__(1024)
-row_plan_kernel(const double* __restrict__ hs, int64_t n, const double* __restrict__ thr, int U,
-                int64_t* __restrict__ rb, int64_t* __restrict__ item_off,
-                uint32_t* __restrict__ guide) {
-  __shared__ uint16_t s_g[kGuide + 1];
-  for (int k = threadIdx.x; k <= U + 1; k += blockDim.x) {
-    int64_t pos;
-    if (k == 0) pos = 0;
-    else if (k == U + 1) pos = n;
-    else {                                  // upper_bound(u[k-1]) over sorted hardness
-      const double u = thr[k - 1];
-      int64_t lo = 0, hi = n;
-      while (lo < hi) { const int64_t mid = (lo + hi) >> 1; if (hs[mid] <= u) lo = mid + 1; else hi = mid; }
-      pos = lo;
-    }
-    rb[k] = pos;
-  }
-  // g(j) = #{u <= j / kGuide}; guide[j] packs (g(j), g(j+1)): for s in
-  // [j/G, (j+1)/G), bs = #{u <= s} lies in [g(j), g(j+1)]
-  for (int j = threadIdx.x; j <= kGuide; j += blockDim.x) {
-    const double x = (double)j / kGuide;
-    int lo = 0, hi = U;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (thr[mid] <= x) lo = mid + 1; else hi = mid; }
-    s_g[j] = (uint16_t)lo;
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j <= kGuide; j += blockDim.x)
-    guide[j] = (uint32_t)s_g[j] | ((uint32_t)s_g[j < kGuide ? j + 1 : kGuide] << 16);
-  // item_off = exclusive prefix of per-row chunk counts (block-wide, chunked)
-  __shared__ int64_t s_carry;
-  __shared__ int64_t s_warp[32];
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base <= U; base += blockDim.x) {
-    const int k = base + threadIdx.x;
-    int64_t v = 0;
-    if (k <= U) { const int64_t len = rb[k + 1] - rb[k]; v = len > 0 ? ceil_div(len, kRowChunk) : 0; }
-    int64_t incl = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += o;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int64_t o = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += o;
-      }
-      s_warp[lane] = w;
-    }
-    __syncthreads();
-    const int64_t excl = s_carry + (warp > 0 ? s_warp[warp - 1] : 0) + incl - v;
-    if (k <= U) item_off[k] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) item_off[U + 1] = s_carry;
+static size_t row_plan_size() {
+  return align256(4 * kMaxBins) * 2 + align256(8 * (kMaxBins + 1)) * 2 + align256(8 * kMaxBins) +
+         align256(kMaxBins) + align256(4 * (kGuide + 1)) * 2 + align256(4);
 }
 
-// #{u <= s} via the guide table (s in [0, 1]) or binary search otherwise
-__device__ __forceinline__ int score_bin(const double* u, int U, const uint32_t* guide, double s) {
-  const int jg = __double2int_rz(s * kGuide);
-  if ((unsigned)jg <= (unsigned)kGuide && s == s) {   // s in [0, 1] (clip output) and not NaN
+// #{u < x} (kLE = false) or #{u <= x} (kLE = true) over sorted unique u, with
+// a guide table g(j) = #{u op j/G} packed as (g(j), g(j+1)): for x in
+// [j/G, (j+1)/G) the answer lies in [g(j), g(j+1)].  x*G is exact (G = 2^12).
+template <bool kLE>
+__device__ __forceinline__ int guided_bin(const double* u, int U, const uint32_t* guide, double x) {
+  if (x >= 0.0 && x <= 1.0) {
+    const int jg = __double2int_rz(x * kGuide);
     const uint32_t gj = guide[jg];
     int lo = (int)(gj & 0xffffu), hi = (int)(gj >> 16);
     if (hi - lo <= 4) {
-      while (lo < hi && u[lo] <= s) ++lo;
+      while (lo < hi && (kLE ? u[lo] <= x : u[lo] < x)) ++lo;
       return lo;
     }
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (u[mid] <= s) lo = mid + 1; else hi = mid; }
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (kLE ? u[mid] <= x : u[mid] < x) lo = mid + 1; else hi = mid;
+    }
     return lo;
   }
-  return count_less_equal(u, U, s);
+  return kLE ? count_less_equal(u, U, x) : count_less(u, U, x);
 }
 
-// grid: (light slots, item slots) -- the models of one chunk are adjacent CTAs,
-// so the chunk's hardness is read from HBM once and from L2 by the others.
-// Hardness (pre-scaled to fixed point at ingest) is accumulated relative to
-// the chunk's smallest value: when the chunk's span fits 32 bits, two 16-bit
-// limbs suffice (3 ATOMS per update), else three (4 ATOMS).  Bin arrays use a
-// compile-time stride so the limb atomics share one address register.
-constexpr int kBinStride = 2048;      // supports up to 2047 distinct thresholds here
+// B0: guides (one thread per bucket) + zero the counters
+__global__ void bucket_setup_kernel(const double* __restrict__ thr, int U, RowPlan rp) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < kMaxBins) rp.row_cnt[j] = 0;
+  if (j == 0) *rp.bad = 0;
+  if (j > kGuide + 1) return;
+  auto cnt = [&](double x, bool le) {
+    int lo = 0, hi = U;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (le ? thr[mid] <= x : thr[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  if (j <= kGuide) {
+    const double x0 = (double)j / kGuide;
+    const double x1 = (double)(j < kGuide ? j + 1 : kGuide) / kGuide;
+    rp.guide_lt[j] = (uint32_t)cnt(x0, false) | ((uint32_t)cnt(x1, false) << 16);
+    rp.guide_le[j] = (uint32_t)cnt(x0, true) | ((uint32_t)cnt(x1, true) << 16);
+  }
+}
+
+// B1: row counts
+__global__ void __launch_bounds__(kCountThreads)
+bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __restrict__ thr, int U,
+                    RowPlan rp) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);             // [kMaxBins]
+  uint32_t* s_guide = s_cnt + kMaxBins;                            // [kGuide + 1]
+  double* s_thr = reinterpret_cast<double*>(s_guide + kGuide + 2); // [U]
+  for (int i = threadIdx.x; i <= U; i += blockDim.x) s_cnt[i] = 0;
+  for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) s_guide[i] = rp.guide_lt[i];
+  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+  __syncthreads();
+  uint32_t my_bad = 0;
+  const int64_t n2 = n >> 1;
+  const double2* h2 = reinterpret_cast<const double2*>(h);
+  const bool vec = (reinterpret_cast<uintptr_t>(h) & 15) == 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto one = [&](double x) {
+    my_bad += !(x >= 0.0 && x <= 1.0);
+    atomicAdd(&s_cnt[guided_bin<false>(s_thr, U, s_guide, x)], 1u);
+  };
+  if (vec) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+      const double2 v = h2[i];
+      one(v.x);
+      one(v.y);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) one(h[n - 1]);
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) one(h[i]);
+  }
+  if (my_bad) atomicAdd(rp.bad, my_bad);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= U; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&rp.row_cnt[i], s_cnt[i]);
+}
+
+// block-wide exclusive scan of one int64 per thread (blockDim.x <= 1024)
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* s_warp, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    s_warp[lane] = w;
+  }
+  __syncthreads();
+  const int64_t excl = (warp > 0 ? s_warp[warp - 1] : 0) + incl - v;
+  *total = s_warp[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return excl;
+}
+
+// B2: row offsets, cursors, K1 items and fixed-point row bounds (one CTA of 1024)
+__global__ void __launch_bounds__(1024)
+bucket_plan_kernel(const double* __restrict__ thr, int U, double hscale, RowPlan rp) {
+  __shared__ int64_t s_warp[32];
+  __shared__ int64_t s_carry[2];
+  if (threadIdx.x == 0) { s_carry[0] = 0; s_carry[1] = 0; }
+  __syncthreads();
+  for (int base = 0; base <= U; base += blockDim.x) {
+    const int k = base + threadIdx.x;
+    const int64_t c = k <= U ? (int64_t)rp.row_cnt[k] : 0;
+    const int64_t items = c > 0 ? ceil_div(c, kRowChunk) : 0;
+    int64_t tot_c, tot_i;
+    const int64_t ec = block_excl_scan(c, s_warp, &tot_c);
+    const int64_t ei = block_excl_scan(items, s_warp, &tot_i);
+    if (k <= U) {
+      const int64_t off = s_carry[0] + ec;
+      rp.row_off[k] = off;
+      rp.cursor[k] = (uint32_t)off;
+      rp.item_off[k] = s_carry[1] + ei;
+      // h in (u[k-1], u[k]] (row 0: [0, u[0]], row U: (u[U-1], 1]) -> hfix bounds
+      const double lo_h = k == 0 ? 0.0 : fmin(fmax(thr[k - 1], 0.0), 1.0);
+      const double hi_h = k == U ? 1.0 : fmin(fmax(thr[k], 0.0), 1.0);
+      const uint64_t lo = (uint64_t)__dmul_rn(lo_h, hscale);
+      const uint64_t hi = (uint64_t)__dmul_rn(fmax(hi_h, lo_h), hscale);
+      rp.row_base[k] = lo;
+      rp.row_narrow[k] = (hi - lo) < (1ull << 32);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { s_carry[0] += tot_c; s_carry[1] += tot_i; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { rp.row_off[U + 1] = s_carry[0]; rp.item_off[U + 1] = s_carry[1]; }
+}
+
+// B3: scatter.  Tile t covers records [t*kBkTile, (t+1)*kBkTile); thread i
+// owns records tile0 + 2*(j*kBkThreads + i) + {0, 1}, j < kBkPer/2, so each
+// warp load is one 512-byte 128-bit-per-lane transaction.
+template <bool kVec>
+__global__ void __launch_bounds__(kBkThreads, 2)
+bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
+                      int n_light, const double* __restrict__ thr, int U, double hscale,
+                      RowPlan rp, uint32_t* __restrict__ hfix_rows, uint16_t* __restrict__ bs_rows) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_gpos = reinterpret_cast<uint32_t*>(smem);       // [kBkTile] sorted -> global pos
+  uint32_t* s_stage = s_gpos + kBkTile;                        // [kBkTile]
+  uint32_t* s_cnt = s_stage + kBkTile;                         // [kMaxBins]
+  uint32_t* s_gbase = s_cnt + kMaxBins;                        // [kMaxBins]
+  uint32_t* s_guide_lt = s_gbase + kMaxBins;                   // [kGuide + 1]
+  uint32_t* s_guide_le = s_guide_lt + (kGuide + 2);            // [kGuide + 1]
+  double* s_thr = reinterpret_cast<double*>(s_guide_le + (kGuide + 2));   // [U]
+  __shared__ int64_t s_warp[32];
+  __shared__ uint32_t s_tile_n;
+  for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) {
+    s_guide_lt[i] = rp.guide_lt[i];
+    s_guide_le[i] = rp.guide_le[i];
+  }
+  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+  const int B1 = U + 1;
+  const int64_t tiles = ceil_div(n, kBkTile);
+  constexpr int kP = kBkPer / 2;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t t0 = tile * kBkTile;
+    const int tn = (int)min((int64_t)kBkTile, n - t0);
+    for (int i = threadIdx.x; i < B1; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    // 1. bin + local rank (ATOMS returns the rank within the tile's row)
+    uint32_t key[kBkPer];          // (row << 16) | rank, 0xffffffff = no record
+    uint64_t hf[kBkPer];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const int r = 2 * (j * kBkThreads + threadIdx.x);
+      double x0 = 0.0, x1 = 0.0;
+      if (kVec && r + 1 < tn) {
+        const double2 v = *reinterpret_cast<const double2*>(h + t0 + r);
+        x0 = v.x; x1 = v.y;
+      } else {
+        if (r < tn) x0 = h[t0 + r];
+        if (r + 1 < tn) x1 = h[t0 + r + 1];
+      }
+      const double xs[2] = {x0, x1};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (r + e < tn) {
+          const double x = xs[e];
+          const int b = guided_bin<false>(s_thr, U, s_guide_lt, x);
+          const uint32_t rank = atomicAdd(&s_cnt[b], 1u);
+          key[2 * j + e] = ((uint32_t)b << 16) | rank;
+          hf[2 * j + e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
+        } else {
+          key[2 * j + e] = 0xffffffffu;
+          hf[2 * j + e] = 0;
+        }
+      }
+    }
+    __syncthreads();
+    // 2. local exclusive offsets + one global reservation per non-empty row
+    {
+      const int per = (B1 + blockDim.x - 1) / blockDim.x;
+      const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+      int64_t tsum = 0;
+      for (int i = i0; i < i1; ++i) tsum += s_cnt[i];
+      int64_t total;
+      int64_t run = block_excl_scan(tsum, s_warp, &total);
+      for (int i = i0; i < i1; ++i) {
+        const uint32_t c = s_cnt[i];
+        s_gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
+        s_cnt[i] = (uint32_t)run;          // s_cnt now holds the local row offsets
+        run += c;
+      }
+      if (threadIdx.x == 0) s_tile_n = (uint32_t)total;
+    }
+    __syncthreads();
+    // 3. sorted slot per record; global position per slot; hfix low half
+#pragma unroll
+    for (int e = 0; e < kBkPer; ++e) {
+      if (key[e] != 0xffffffffu) {
+        const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
+        const uint32_t slot = s_cnt[b] + rank;
+        s_gpos[slot] = s_gbase[b] + rank;
+        s_stage[slot] = (uint32_t)hf[e];
+        key[e] = slot;
+      }
+    }
+    __syncthreads();
+    const int cnt = (int)s_tile_n;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) hfix_rows[2 * (int64_t)s_gpos[i]] = s_stage[i];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < kBkPer; ++e)
+      if (key[e] != 0xffffffffu) s_stage[key[e]] = (uint32_t)(hf[e] >> 32);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      hfix_rows[2 * (int64_t)s_gpos[i] + 1] = s_stage[i];
+    // 4. per light model: tau-bins, staged into row order
+    uint16_t* s_st16 = reinterpret_cast<uint16_t*>(s_stage);
+    for (int l = 0; l < n_light; ++l) {
+      const double* srow = scores + (int64_t)l * n + t0;
+      double sv[kBkPer];
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        const int r = 2 * (j * kBkThreads + threadIdx.x);
+        if (kVec && r + 1 < tn) {
+          const double2 v = *reinterpret_cast<const double2*>(srow + r);
+          sv[2 * j] = v.x; sv[2 * j + 1] = v.y;
+        } else {
+          sv[2 * j] = r < tn ? srow[r] : 0.0;
+          sv[2 * j + 1] = r + 1 < tn ? srow[r + 1] : 0.0;
+        }
+      }
+      __syncthreads();       // previous model's stage fully written out
+#pragma unroll
+      for (int e = 0; e < kBkPer; ++e)
+        if (key[e] != 0xffffffffu)
+          s_st16[key[e]] = (uint16_t)guided_bin<true>(s_thr, U, s_guide_le, sv[e]);
+      __syncthreads();
+      uint16_t* orow = bs_rows + (int64_t)l * n;
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) orow[s_gpos[i]] = s_st16[i];
+    }
+    __syncthreads();
+  }
+}
+
+// K1: grid (light slots, items).  The light models of one item are adjacent
+// CTAs, so the item's hfix run is read from HBM once and from L2 by the rest.
+constexpr int kBinStride = kMaxBins;
 
 template <bool kNarrow>
 __global__ void __launch_bounds__(kK1Threads)
-row_hist_kernel(const unsigned long long* __restrict__ hf, const double* __restrict__ ss, int64_t n,
-                const double* __restrict__ thr, int U, const uint32_t* __restrict__ g_guide,
-                const int64_t* __restrict__ rb, const int64_t* __restrict__ item_off,
-                const uint8_t* __restrict__ item_narrow, uint32_t* __restrict__ g_cnt,
-                unsigned long long* __restrict__ g_hsum, uint8_t* __restrict__ row_scanned) {
-  extern __shared__ __align__(16) unsigned char smem[];
+row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs, int64_t n, int U,
+                RowPlan rp, uint32_t* __restrict__ g_cnt, unsigned long long* __restrict__ g_hsum,
+                uint8_t* __restrict__ row_scanned) {
+  __shared__ uint32_t s_bin[4 * kBinStride];
   const int B1 = U + 1;
-  uint32_t* s_bin = reinterpret_cast<uint32_t*>(smem);          // [4][kBinStride]
-  double* s_thr = reinterpret_cast<double*>(s_bin + 4 * kBinStride);
-  uint32_t* s_guide = reinterpret_cast<uint32_t*>(s_thr + U);
-  const int64_t items = item_off[U + 1];
+  const int64_t items = rp.item_off[U + 1];
   const int64_t item = blockIdx.y;
-  if (item >= items || (item_narrow[item] != 0) != kNarrow) return;
+  if (item >= items) return;
   int lo = 0, hi = U + 1;
-  while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (item_off[mid] <= item) lo = mid; else hi = mid - 1; }
+  while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (rp.item_off[mid] <= item) lo = mid; else hi = mid - 1; }
   const int k = lo;
-  const int64_t chunk = item - item_off[k];
-  const int64_t r0 = rb[k] + chunk * kRowChunk;
-  const int64_t r1 = min(rb[k + 1], r0 + kRowChunk);
-  const bool whole_row = (r0 == rb[k]) && (r1 == rb[k + 1]);
+  if ((rp.row_narrow[k] != 0) != kNarrow) return;
+  const int64_t chunk = item - rp.item_off[k];
+  const int64_t r0 = rp.row_off[k] + chunk * kRowChunk;
+  const int64_t r1 = min(rp.row_off[k + 1], r0 + kRowChunk);
+  const bool whole_row = (r0 == rp.row_off[k]) && (r1 == rp.row_off[k + 1]);
   const int l = blockIdx.x;
-  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
-  for (int i = threadIdx.x; i < 4 * kBinStride; i += blockDim.x) s_bin[i] = 0;
-  for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) s_guide[i] = g_guide[i];
+  for (int i = threadIdx.x; i < (kNarrow ? 3 : 4) * kBinStride; i += blockDim.x) s_bin[i] = 0;
   __syncthreads();
-  const double* srow = ss + (int64_t)l * n;
-  const unsigned long long base = hf[r0];
-  constexpr int kU = 4;
-  int64_t q = r0 + threadIdx.x;
-  for (; q + (kU - 1) * (int64_t)blockDim.x < r1; q += kU * (int64_t)blockDim.x) {
-    unsigned long long hv[kU];
-    double sv[kU];
-#pragma unroll
-    for (int j = 0; j < kU; ++j) { hv[j] = hf[q + j * blockDim.x]; sv[j] = srow[q + j * blockDim.x]; }
-#pragma unroll
-    for (int j = 0; j < kU; ++j) {
-      const unsigned long long d = hv[j] - base;
-      uint32_t* a = s_bin + score_bin(s_thr, U, s_guide, sv[j]);
-      atomicAdd(a, 1u);
-      atomicAdd(a + kBinStride, (uint32_t)(d & 0xffffu));
-      atomicAdd(a + 2 * kBinStride, (uint32_t)((d >> 16) & 0xffffu));
-      if (!kNarrow) atomicAdd(a + 3 * kBinStride, (uint32_t)(d >> 32));
-    }
-  }
-  for (; q < r1; q += blockDim.x) {
-    const unsigned long long d = hf[q] - base;
-    uint32_t* a = s_bin + score_bin(s_thr, U, s_guide, srow[q]);
+  const uint16_t* brow = bs + (int64_t)l * n;
+  const unsigned long long base = rp.row_base[k];
+  auto add = [&](unsigned long long hv, int b) {
+    const unsigned long long d = hv - base;
+    uint32_t* a = s_bin + b;
     atomicAdd(a, 1u);
     atomicAdd(a + kBinStride, (uint32_t)(d & 0xffffu));
     atomicAdd(a + 2 * kBinStride, (uint32_t)((d >> 16) & 0xffffu));
     if (!kNarrow) atomicAdd(a + 3 * kBinStride, (uint32_t)(d >> 32));
+  };
+  constexpr int kU = 4;
+  int64_t q = r0 + threadIdx.x;
+  for (; q + (kU - 1) * (int64_t)blockDim.x < r1; q += kU * (int64_t)blockDim.x) {
+    unsigned long long hv[kU];
+    int bv[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) { hv[j] = hf[q + j * blockDim.x]; bv[j] = brow[q + j * blockDim.x]; }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) add(hv[j], bv[j]);
   }
+  for (; q < r1; q += blockDim.x) add(hf[q], brow[q]);
   __syncthreads();
   uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
   unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
   auto bin_sum = [&](int i) {
-    return (unsigned long long)s_bin[i] * base + (unsigned long long)s_bin[kBinStride + i] +
-           ((unsigned long long)s_bin[2 * kBinStride + i] << 16) +
-           ((unsigned long long)s_bin[3 * kBinStride + i] << 32);
+    unsigned long long v = (unsigned long long)s_bin[i] * base + (unsigned long long)s_bin[kBinStride + i] +
+                           ((unsigned long long)s_bin[2 * kBinStride + i] << 16);
+    if (!kNarrow) v += (unsigned long long)s_bin[3 * kBinStride + i] << 32;
+    return v;
   };
   if (!whole_row || !row_scanned) {
     for (int i = threadIdx.x; i < B1; i += blockDim.x) {
@@ -262,105 +461,82 @@ row_hist_kernel(const unsigned long long* __restrict__ hf, const double* __restr
   if (threadIdx.x == 0) row_scanned[(int64_t)l * B1 + k] = 1;
 }
 
-// per item: does its hardness span fit 32 bits (narrow) ?
-__global__ void item_span_kernel(const unsigned long long* __restrict__ hf, int U,
-                                 const int64_t* __restrict__ rb,
-                                 const int64_t* __restrict__ item_off, int64_t max_items,
-                                 uint8_t* __restrict__ item_narrow) {
-  const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= max_items) return;
-  if (item >= item_off[U + 1]) { item_narrow[item] = 0; return; }
-  int lo = 0, hi = U + 1;
-  while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (item_off[mid] <= item) lo = mid; else hi = mid - 1; }
-  const int64_t r0 = rb[lo] + (item - item_off[lo]) * kRowChunk;
-  const int64_t r1 = min(rb[lo + 1], r0 + kRowChunk);
-  item_narrow[item] = hf[r1 - 1] - hf[r0] < (1ull << 32);
+static size_t scatter_smem(int U) {
+  return (size_t)4 * (2 * kBkTile + 2 * kMaxBins + 2 * (kGuide + 2)) + (size_t)8 * U;
 }
 
 }  // namespace hadis
 
 using namespace hadis;
 
-extern "C" size_t hadis_records_workspace_bytes(int64_t n) {
-  if (n <= 0) return 0;
-  return sort_workspace_bytes(n);
+extern "C" size_t hadis_row_plan_bytes(int32_t n_unique) {
+  if (n_unique <= 0 || n_unique + 1 > kMaxBins) return 0;
+  return row_plan_size();
 }
 
-extern "C" int hadis_records_sort(const double* h, const double* scores, int64_t n, int32_t n_rows,
-                                  int32_t hfix_shift, double* h_sorted, uint64_t* hfix_sorted,
-                                  double* scores_sorted, uint32_t* perm, uint32_t* bad_records,
-                                  void* workspace, size_t workspace_bytes, void* stream) {
-  if (!h || n <= 0 || n > 0xffffffffll || n_rows < 0 || (n_rows > 0 && (!scores || !scores_sorted))
-      || !h_sorted || !hfix_sorted || !bad_records || !workspace || hfix_shift < 1 ||
-      hfix_shift > 48)
+extern "C" int hadis_records_bucket(const double* h, const double* scores, int64_t n,
+                                    int32_t n_light, const double* thr_unique, int32_t n_unique,
+                                    int32_t hfix_shift, uint64_t* hfix_rows, uint16_t* bs_rows,
+                                    uint32_t* bad_records, void* row_plan, size_t row_plan_bytes,
+                                    void* stream) {
+  if (!h || n <= 0 || n > 0xffffffffll || n_light < 0 || (n_light > 0 && (!scores || !bs_rows)) ||
+      !thr_unique || n_unique <= 0 || !hfix_rows || !row_plan || hfix_shift < 1 || hfix_shift > 48)
     return HADIS_ERR_ARG;
-  if (workspace_bytes < hadis_records_workspace_bytes(n)) return HADIS_ERR_CAPACITY;
+  if (n_unique + 1 > kMaxBins) return HADIS_ERR_UNSUPPORTED;
+  if (row_plan_bytes < row_plan_size()) return HADIS_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
-  HADIS_CUDA_TRY(cudaMemsetAsync(bad_records, 0, 4, st));
-  const uint32_t* idx = nullptr;
-  const int rc = sort_keys(h, nullptr, n, workspace, st, &idx, nullptr);
-  if (rc != HADIS_OK) return rc;
-  int64_t grid = ceil_div(n, 256);
-  if (grid > kNumSMs * 8) grid = kNumSMs * 8;
-  gather_kernel<<<(unsigned)grid, 256, 0, st>>>(h, scores, n, n_rows, idx, ldexp(1.0, hfix_shift),
-                                                h_sorted, (unsigned long long*)hfix_sorted,
-                                                scores_sorted, perm, bad_records);
+  const RowPlan rp = row_plan_at(row_plan);
+  const double hscale = ldexp(1.0, hfix_shift);
+  bucket_setup_kernel<<<(unsigned)ceil_div(kGuide + 2, 256), 256, 0, st>>>(thr_unique, n_unique, rp);
   HADIS_LAUNCH_CHECK();
-  hadis_count_launches(1);
+  const size_t csmem = (size_t)4 * (kMaxBins + kGuide + 2) + (size_t)8 * n_unique;
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_count_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  int64_t cgrid = ceil_div(n, 2 * kCountThreads * 8);
+  if (cgrid > kNumSMs * 2) cgrid = kNumSMs * 2;
+  bucket_count_kernel<<<(unsigned)cgrid, kCountThreads, csmem, st>>>(h, n, thr_unique, n_unique, rp);
+  HADIS_LAUNCH_CHECK();
+  bucket_plan_kernel<<<1, 1024, 0, st>>>(thr_unique, n_unique, hscale, rp);
+  HADIS_LAUNCH_CHECK();
+  const size_t ssmem = scatter_smem(n_unique);
+  bool vec = (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (n & 1) == 0 &&
+             (n_light == 0 || (reinterpret_cast<uintptr_t>(scores) & 15) == 0);
+  auto kern = vec ? bucket_scatter_kernel<true> : bucket_scatter_kernel<false>;
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+  int64_t sgrid = ceil_div(n, kBkTile);
+  if (sgrid > kNumSMs * 2) sgrid = kNumSMs * 2;
+  kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
+                                                   hscale, rp, (uint32_t*)hfix_rows, bs_rows);
+  HADIS_LAUNCH_CHECK();
+  if (bad_records)
+    HADIS_CUDA_TRY(cudaMemcpyAsync(bad_records, rp.bad, 4, cudaMemcpyDeviceToDevice, st));
+  hadis_count_launches(4);
   return HADIS_OK;
 }
 
-static int64_t k1_max_items(int64_t n, int32_t n_unique) {
-  return ceil_div(n, kRowChunk) + n_unique + 1;
-}
-
-extern "C" size_t hadis_bin_hist_sorted_workspace_bytes(int64_t n, int32_t n_unique) {
-  if (n <= 0 || n_unique <= 0) return 0;
-  return (size_t)8 * (2 * (size_t)n_unique + 4) + 4 * (kGuide + 1) +
-         (size_t)k1_max_items(n, n_unique) + 256;
-}
-
-extern "C" int hadis_bin_hist_sorted(const double* h_sorted, const uint64_t* hfix_sorted,
-                                     const double* scores_sorted, int64_t n, int32_t n_light,
-                                     const double* thr_unique, int32_t n_unique,
-                                     uint32_t* hist_cnt, uint64_t* hist_hsum, uint8_t* row_scanned,
-                                     void* workspace, size_t workspace_bytes, void* stream) {
-  if (!h_sorted || !hfix_sorted || !scores_sorted || n <= 0 || n > 0xffffffffll || n_light <= 0 ||
-      n_unique <= 0 || !thr_unique || !hist_cnt || !hist_hsum || !workspace || n_light > 65535)
+extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs_rows, int64_t n,
+                                   int32_t n_light, int32_t n_unique, const void* row_plan,
+                                   uint32_t* hist_cnt, uint64_t* hist_hsum, uint8_t* row_scanned,
+                                   void* stream) {
+  if (!hfix_rows || !bs_rows || n <= 0 || n > 0xffffffffll || n_light <= 0 || n_unique <= 0 ||
+      !row_plan || !hist_cnt || !hist_hsum || n_light > 65535)
     return HADIS_ERR_ARG;
-  if (n_unique + 1 > kBinStride) return HADIS_ERR_UNSUPPORTED;
-  if (workspace_bytes < hadis_bin_hist_sorted_workspace_bytes(n, n_unique))
-    return HADIS_ERR_CAPACITY;
+  if (n_unique + 1 > kMaxBins) return HADIS_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
+  const RowPlan rp = row_plan_at(const_cast<void*>(row_plan));
   const int64_t B1 = (int64_t)n_unique + 1;
-  int64_t* rb = (int64_t*)workspace;
-  int64_t* item_off = rb + (n_unique + 2);
-  uint32_t* guide = (uint32_t*)(item_off + (n_unique + 2));
-  uint8_t* item_narrow = (uint8_t*)(guide + (kGuide + 1));
   const int64_t bins = B1 * B1 * n_light;
-  const int64_t max_items = k1_max_items(n, n_unique);
+  const int64_t max_items = ceil_div(n, kRowChunk) + n_unique + 1;
   if (max_items > 65535) return HADIS_ERR_UNSUPPORTED;
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
   if (row_scanned) HADIS_CUDA_TRY(cudaMemsetAsync(row_scanned, 0, (size_t)B1 * n_light, st));
-  row_plan_kernel<<<1, 1024, 0, st>>>(h_sorted, n, thr_unique, n_unique, rb, item_off, guide);
-  item_span_kernel<<<(unsigned)ceil_div(max_items, 256), 256, 0, st>>>(
-      (const unsigned long long*)hfix_sorted, n_unique, rb, item_off, max_items, item_narrow);
-  HADIS_LAUNCH_CHECK();
-  const size_t smem = (size_t)4 * kBinStride * 4 + (size_t)n_unique * 8 + 4 * (kGuide + 1) + 16;
-  if (smem > 227 * 1024) return HADIS_ERR_UNSUPPORTED;
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid((unsigned)n_light, (unsigned)max_items);
-  row_hist_kernel<true><<<grid, kK1Threads, smem, st>>>(
-      (const unsigned long long*)hfix_sorted, scores_sorted, n, thr_unique, n_unique, guide, rb,
-      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum, row_scanned);
-  row_hist_kernel<false><<<grid, kK1Threads, smem, st>>>(
-      (const unsigned long long*)hfix_sorted, scores_sorted, n, thr_unique, n_unique, guide, rb,
-      item_off, item_narrow, hist_cnt, (unsigned long long*)hist_hsum, row_scanned);
+  row_hist_kernel<true><<<grid, kK1Threads, 0, st>>>(hfix_rows, bs_rows, n, n_unique, rp, hist_cnt,
+                                                    (unsigned long long*)hist_hsum, row_scanned);
+  row_hist_kernel<false><<<grid, kK1Threads, 0, st>>>(hfix_rows, bs_rows, n, n_unique, rp, hist_cnt,
+                                                     (unsigned long long*)hist_hsum, row_scanned);
   HADIS_LAUNCH_CHECK();
-  hadis_count_launches(4);
+  hadis_count_launches(2);
   return HADIS_OK;
 }

@@ -264,7 +264,7 @@ class GridProfiler:
     ``run`` profiles one threshold grid; ``launch``/``finish`` split it into an
     asynchronous enqueue and a synchronising check for pipelined callers."""
 
-    def __init__(self, pool, h, scores, device=None, layout="sorted"):
+    def __init__(self, pool, h, scores, device=None, layout="bucketed"):
         torch = _lib.torch_cuda()
         self.torch = torch
         self.pool = list(pool)
@@ -283,32 +283,23 @@ class GridProfiler:
         self.shift = self.lib.hadis_hfix_shift(self.n)
         self._ws = None
         self._plans = {}
-        if layout not in ("sorted", "original"):
-            raise ValueError("layout must be 'sorted' or 'original'")
+        if layout not in ("bucketed", "original"):
+            raise ValueError("layout must be 'bucketed' or 'original'")
         self.layout = layout
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
-        if layout == "sorted":
-            self.ingest()
+        self._store = None
 
-    def ingest(self, stream=None):
-        """Record-store layout: hardness-sorted copies of h and the score rows
-        (hadis_records_sort).  K1 then reads each threshold row as a contiguous
-        run; the original-order arrays stay for the exact-fidelity emulation."""
+    def _bucket_store(self, n_light):
+        """Row-bucketed record store buffers (hfix u64[n], bs u16[n_light][n], row plan)."""
         torch = self.torch
-        L = int(self.scores.shape[0])
-        self.hs = torch.empty_like(self.h)
-        self.hfs = torch.empty(self.n, dtype=torch.int64, device=self.device)
-        self.ss = torch.empty_like(self.scores)
-        ws_bytes = self.lib.hadis_records_workspace_bytes(self.n)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
-        p = _lib.ptr
-        _lib.check(self.lib.hadis_records_sort(p(self.h), p(self.scores), self.n, L, self.shift,
-                                               p(self.hs), p(self.hfs), p(self.ss), None,
-                                               p(self.bad), p(ws), ws_bytes,
-                                               _lib.stream_handle(stream)), "hadis_records_sort")
-        k1 = self.lib.hadis_bin_hist_sorted_workspace_bytes(self.n, 2047)
-        self._k1_ws = torch.empty(max(1, k1), dtype=torch.uint8, device=self.device)
-        del ws
+        st = self._store
+        if st is None or st[1].shape[0] < n_light:
+            st = self._store = (torch.empty(self.n, dtype=torch.int64, device=self.device),
+                                torch.empty((n_light, self.n), dtype=torch.int16,
+                                            device=self.device),
+                                torch.empty(self.lib.hadis_row_plan_bytes(1), dtype=torch.uint8,
+                                            device=self.device))
+        return st
 
     def plan(self, thresholds=THRESHOLD_GRID, pairs=None) -> ProfilePlan:
         key = (tuple(float(t) for t in thresholds), None if pairs is None else tuple(pairs))
@@ -322,9 +313,9 @@ class GridProfiler:
         return self.finish(self.launch(self.plan(thresholds, pairs), exact_fid, stream))
 
     def launch(self, plan: ProfilePlan, exact_fid=False, stream=None, events=None):
-        """Enqueue K1 (bin + histogram), K2 (2-D scan) and K3/K4 (frontier) on
-        ``stream``; no host synchronisation.  ``events`` (optional list of 4
-        torch.cuda.Event) brackets K1 | K2 | K3+K4 for per-kernel timing."""
+        """Enqueue B (row-bucketed record store), K1 (histogram), K2 (2-D scan)
+        and K3/K4 (frontier) on ``stream``; no host synchronisation.  ``events``
+        (optional list of 5 torch.cuda.Event) brackets B | K1 | K2 | K3+K4."""
         torch = self.torch
         dev = self.device
         st = _lib.stream_handle(stream)
@@ -338,24 +329,29 @@ class GridProfiler:
         p = _lib.ptr
         rec = (lambda i: events[i].record(stream)) if events is not None else (lambda i: None)
         rec(0)
-        if self.layout == "sorted" and plan.U < 2048:
-            ss = self.ss[plan.slot0:plan.slot0 + plan.n_light]
-            _lib.check(self.lib.hadis_bin_hist_sorted(
-                p(self.hs), p(self.hfs), p(ss), self.n, plan.n_light, p(plan.d_u), plan.U,
-                p(state["cnt"]), p(state["hsum"]), p(state["scanned"]), p(self._k1_ws),
-                self._k1_ws.numel(), st), "hadis_bin_hist_sorted")
+        if self.layout == "bucketed" and plan.U < 2048:
+            hfix, bs, rplan = self._bucket_store(plan.n_light)
+            _lib.check(self.lib.hadis_records_bucket(
+                p(self.h), p(state["scores"]), self.n, plan.n_light, p(plan.d_u), plan.U,
+                self.shift, p(hfix), p(bs), p(self.bad), p(rplan), rplan.numel(), st),
+                "hadis_records_bucket")
+            rec(1)
+            _lib.check(self.lib.hadis_bin_hist_rows(
+                p(hfix), p(bs), self.n, plan.n_light, plan.U, p(rplan), p(state["cnt"]),
+                p(state["hsum"]), p(state["scanned"]), st), "hadis_bin_hist_rows")
             scanned = state["scanned"]
         else:
+            rec(1)
             _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
                                                p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
                                                p(state["hsum"]), p(self.bad), st), "hadis_bin_hist")
             scanned = None
-        rec(1)
+        rec(2)
         _lib.check(self.lib.hadis_hist_scan(p(state["cnt"]), p(state["hsum"]), plan.n_light,
                                             plan.U, p(scanned), st), "hadis_hist_scan")
-        rec(2)
-        self._frontier(state, plan.caps)
         rec(3)
+        self._frontier(state, plan.caps)
+        rec(4)
         return state
 
     def _frontier(self, state, caps):

@@ -252,9 +252,9 @@ def test_c2_scale_properties(gpu_device):
         assert math.isclose(r.fidelity_cost, fid, rel_tol=1e-9)
 
 
-@pytest.mark.parametrize("layout", ["sorted", "original"])
+@pytest.mark.parametrize("layout", ["bucketed", "original"])
 def test_k1_layouts_agree(gpu_device, layout):
-    """Both K1 paths (hardness-sorted record store / original order with L2
+    """Both K1 paths (row-bucketed record store / original order with L2
     atomics) give the same table as the oracle."""
     rng = np.random.default_rng(99)
     cat = default_catalog()
@@ -269,6 +269,50 @@ def test_k1_layouts_agree(gpu_device, layout):
             r.mean_latency_s) for r in rows_from_device(prof.run(thr), pool, thr)]
     want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
     assert_rows_close(got, want)
+
+
+@pytest.mark.parametrize("n,thr_k,shift_case", [(100_001, 48, "odd"), (262_144, 64, "wide"),
+                                                 (3, 5, "tiny"), (70_000, 1024, "k1024")])
+def test_bucketed_histograms_bitexact(gpu_device, n, thr_k, shift_case):
+    """The row-bucketed store + K1 give bit-identical prefix tables to the
+    global-atomic K1 on adversarial records: hardness exactly on thresholds,
+    0.0 and 1.0, one row holding > 32768 records (chunked, atomics), odd n
+    (scalar loads), scores on thresholds and at the clip bounds."""
+    import torch
+    rng = np.random.default_rng(n + thr_k)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    thr = tuple(i / (thr_k - 1) for i in range(thr_k))
+    h = rng.uniform(0.0, 1.0, n)
+    pick = rng.random(n)
+    h[pick < 0.2] = rng.choice(np.asarray(thr), int((pick < 0.2).sum()))
+    h[(pick >= 0.2) & (pick < 0.6)] = thr[len(thr) // 2] + 1e-9   # one heavy row
+    h[pick > 0.98] = 0.0
+    h[pick > 0.99] = 1.0
+    sc = rng.uniform(0.0, 1.0, (len(pool) - 1, n))
+    sc[:, ::7] = rng.choice(np.asarray(thr), sc[:, ::7].shape)
+    sc[:, ::11] = 0.0
+    sc[:, ::13] = 1.0
+    tabs = {}
+    for layout in ("bucketed", "original"):
+        prof = GridProfiler(pool, h, sc, layout=layout)
+        st = prof.launch(prof.plan(thr))
+        prof.finish(st)
+        tabs[layout] = (st["cnt"].clone(), st["hsum"].clone())
+    torch.cuda.synchronize()
+    assert torch.equal(tabs["bucketed"][0], tabs["original"][0])
+    assert torch.equal(tabs["bucketed"][1], tabs["original"][1])
+
+
+def test_bucketed_rejects_bad_hardness(gpu_device):
+    from paper_2509_00642_b200.profiler import ProfileError
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    h = np.linspace(0.0, 1.0, 1000)
+    h[17] = 1.5
+    prof = GridProfiler(pool, h, np.full((len(pool) - 1, 1000), 0.5))
+    with pytest.raises(ProfileError):
+        prof.run((0.0, 0.5, 1.0))
 
 
 @pytest.mark.parametrize("world", [2, 3])
