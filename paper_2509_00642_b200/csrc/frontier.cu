@@ -73,6 +73,17 @@ __device__ __forceinline__ const uint64_t* slot_hs(const Grid& g, int slot) {
   return g.hs + (int64_t)slot * g.B1 * g.B1;
 }
 
+// fid* numerator, the one formula every stage uses (so equal heavy sets give
+// bitwise-equal values):  S = (b_h nH + p_h SH 2^-s) + (b_l nL + p_l SL 2^-s).
+// The light part depends on the light model only, so row passes stage it
+// once per cell for all heavy partners.  SH 2^-s is exact (power of two).
+__device__ __forceinline__ double light_part(double bl, double pl, double dnL, double dSLs) {
+  return __dadd_rn(__dmul_rn(bl, dnL), __dmul_rn(pl, dSLs));
+}
+__device__ __forceinline__ double fid_num(double bh, double ph, double dnH, double dSHs, double lp) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(bh, dnH), __dmul_rn(ph, dSHs)), lp);
+}
+
 __device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc, int k, int t) {
   const uint32_t* C = slot_cnt(g, pc.slot);
   const uint64_t* S = slot_hs(g, pc.slot);
@@ -91,10 +102,8 @@ __device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc,
   v.n_heavy = nH;
   const double dn = (double)g.n;
   v.lat = __ddiv_rn(__dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh)), dn);
-  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)SH), __dmul_rn(pc.pl, (double)SL)),
-                                 g.inv_scale);
-  const double base = __dadd_rn(__dmul_rn(pc.bh, (double)nH), __dmul_rn(pc.bl, (double)(n - nH)));
-  v.fid = __ddiv_rn(__dadd_rn(base, hterm), dn);
+  const double lp = light_part(pc.bl, pc.pl, (double)(n - nH), __dmul_rn((double)SL, g.inv_scale));
+  v.fid = __ddiv_rn(fid_num(pc.bh, pc.ph, (double)nH, __dmul_rn((double)SH, g.inv_scale), lp), dn);
   return v;
 }
 
@@ -112,9 +121,8 @@ __device__ __forceinline__ void cell_numerators(const Grid& g, const PairConst& 
   const uint64_t SH = (Htot - Sh[rk + g.U]) + Sh[rk + t];
   const uint64_t SL = Htot - SH;
   *x = __dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh));
-  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, (double)SH), __dmul_rn(pc.pl, (double)SL)),
-                                 g.inv_scale);
-  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, (double)nH), __dmul_rn(pc.bl, (double)(n - nH))), hterm);
+  const double lp = light_part(pc.bl, pc.pl, (double)(n - nH), __dmul_rn((double)SL, g.inv_scale));
+  *S = fid_num(pc.bh, pc.ph, (double)nH, __dmul_rn((double)SH, g.inv_scale), lp);
 }
 
 // Per-(light slot, k, t) integer statistics, shared by every heavy partner.
@@ -144,17 +152,21 @@ __device__ __forceinline__ CellInts cell_ints(const Grid& g, const uint32_t* C, 
 __device__ __forceinline__ void numerators_of(const Grid& g, const PairConst& pc, const CellInts& c,
                                               double* x, double* S) {
   *x = __dadd_rn(__dmul_rn(c.dRk, pc.Ll), __dmul_rn(c.dnH, pc.Lh));
-  const double hterm = __dmul_rn(__dadd_rn(__dmul_rn(pc.ph, c.dSH), __dmul_rn(pc.pl, c.dSL)),
-                                 g.inv_scale);
-  *S = __dadd_rn(__dadd_rn(__dmul_rn(pc.bh, c.dnH), __dmul_rn(pc.bl, c.dnL)), hterm);
+  const double lp = light_part(pc.bl, pc.pl, c.dnL, __dmul_rn(c.dSL, g.inv_scale));
+  *S = fid_num(pc.bh, pc.ph, c.dnH, __dmul_rn(c.dSH, g.inv_scale), lp);
 }
 
 // bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
 __device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, double x) {
-  double b = floor(__dmul_rn(__dadd_rn(x, -pc.lo_x), pc.scale_x));
-  if (!(b >= 0.0)) b = 0.0;
-  if (b > (double)(nbuckets - 1)) b = (double)(nbuckets - 1);
-  return (int)b;
+  // floor + saturating convert in one instruction (NaN -> INT_MIN -> bucket 0)
+  const int b = __double2int_rd(__dmul_rn(__dadd_rn(x, -pc.lo_x), pc.scale_x));
+  return min(max(b, 0), nbuckets - 1);
+}
+
+// order_key without branches (same map as common.cuh's order_key)
+__device__ __forceinline__ unsigned long long order_key_fast(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(__dadd_rn(x, 0.0));
+  return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ull);
 }
 
 __device__ __forceinline__ int bucket_of(const Grid& g, const PairConst& pc, int k, int t) {
@@ -272,42 +284,196 @@ row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
 
 // ---------------------------------------------------------- F1: bucket minima
 
-constexpr int kCellThreads = 256;
 
 // Pairs sharing a light slot are contiguous ("groups"); a thread loads one
 // (slot, k, t) cell's integer statistics once and evaluates every heavy
 // partner of the group.  grid: (cell tiles, group upper bound), x fastest, so
 // one light model's prefix table stays L2-resident while its pairs run.
 __global__ void group_kernel(const int32_t* __restrict__ pair_slot, int n_pairs,
-                             int32_t* __restrict__ group_p0, int32_t* __restrict__ n_groups) {
+                             int32_t* __restrict__ group_p0, int32_t* __restrict__ n_groups,
+                             unsigned long long* counters, int max_group) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   int ng = 0;
   for (int p = 0; p < n_pairs; ++p)
     if (p == 0 || pair_slot[p] != pair_slot[p - 1]) group_p0[ng++] = p;
   group_p0[ng] = n_pairs;
+  for (int i = 0; i < ng; ++i)
+    if (group_p0[i + 1] - group_p0[i] > max_group) {   // > 65 pool models: unsupported
+      counters[4] |= 128ull;
+      ng = 0;
+    }
   *n_groups = ng;
 }
 
-__global__ void __launch_bounds__(kCellThreads)
+struct __align__(16) Cand {
+  uint32_t pair, cell, bucket, pad;   // cell = k * U + t (representative)
+  double lat, fid;
+};
+struct Cands {
+  Cand* c;
+};
+
+// Row passes F1 / F3.  One warp per (light slot, theta rank k); a CTA holds
+// kRowWarps rows of one slot group.  Along a row the latency numerator x is
+// non-decreasing in t (the reject count is), so a cell whose S exceeds the
+// exclusive prefix-min of S over the earlier cells of its row is dominated by
+// one of them (lat <=, fid* <).  The row is walked in windows of kRowWin
+// cells: the warp stages the window's statistics as doubles in shared memory
+// (shared by every heavy partner of the slot); per partner, lane l evaluates
+// its kRowT contiguous cells, one warp scan of the lane minima gives each
+// lane its carry-in, and the per-cell test is one compare.  The [j][33]
+// layout keeps staging stores and per-lane reads conflict-free.  Rows that
+// repeat an earlier row's R[k] (same row class) are exact duplicates and are
+// skipped.
+constexpr int kRowWarps = 8;
+constexpr int kMaxGroup = 64;        // heavy partners per light slot (pool <= 65 models)
+constexpr int kRowT = 8;             // cells per lane per window
+constexpr int kRowWin = 32 * kRowT;  // cells per window
+constexpr int kRowPad = 33;
+
+struct RowSmem {
+  double nH[kRowWarps][kRowT * kRowPad];    // heavy-served records
+  double SHs[kRowWarps][kRowT * kRowPad];   // their hardness sum * 2^-shift
+  double LP[kRowWarps][kRowT * kRowPad];    // light part of the fid* numerator
+  uint8_t cls[kRowWarps][kRowT * kRowPad];  // 1 = first of its duplicate run, 2 = past the end
+  unsigned long long carry[kRowWarps][kMaxGroup];
+  PairConst pc[kMaxGroup];
+};
+
+__device__ __forceinline__ bool row_task(const Grid& g, const PairConst* __restrict__ pcs,
+                                         const int32_t* __restrict__ group_p0,
+                                         const int32_t* __restrict__ n_groups, RowSmem& sm,
+                                         int* p0, int* p1, int* k) {
+  const int grp = blockIdx.y;
+  if (grp >= *n_groups) return false;
+  *p0 = group_p0[grp];
+  *p1 = group_p0[grp + 1];
+  const int np = *p1 - *p0;                      // <= kMaxGroup (checked on the host)
+  for (int i = threadIdx.x; i < np * (int)(sizeof(PairConst) / 8); i += blockDim.x)
+    reinterpret_cast<double*>(sm.pc)[i] = reinterpret_cast<const double*>(pcs + *p0)[i];
+  __syncthreads();
+  *k = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  return *k < g.U && g.row_start[*k];
+}
+
+// visit(p, pc, w0, key[kRowT], take) once per (window, partner), all lanes:
+// lane l owns cells t = w0 + l*kRowT + j; key[j] = order_key(S) (S = +inf past
+// the row end); bit j of take = the cell passes the row test -- strict
+// prefix-min (F1) or class start within 2 delta of the prefix-min (F3).
+template <bool kFilter, typename F>
+__device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0, int p1, int k,
+                                             F&& visit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
+  const uint64_t* Sh = slot_hs(g, sm.pc[0].slot);
+  const int64_t rk = (int64_t)k * g.B1;
+  const uint32_t n = (uint32_t)g.n;
+  const uint32_t Rk = C[rk + g.U];
+  const uint64_t Htot = Sh[(int64_t)g.U * g.B1 + g.U];
+  const uint64_t Hnb = Htot - Sh[rk + g.U];        // hardness of bypassed records
+  const double bl = sm.pc[0].bl, pl = sm.pc[0].pl, inv = g.inv_scale;
+  double* s_nH = sm.nH[warp];
+  double* s_SHs = sm.SHs[warp];
+  double* s_LP = sm.LP[warp];
+  uint8_t* s_cls = sm.cls[warp];
+  {
+    const int q0 = p0, q1 = p1;
+    for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = ~0ull;
+    for (int w0 = 0; w0 < g.U; w0 += kRowWin) {
+      __syncwarp();
+      for (int i = lane; i < kRowWin; i += 32) {       // stage (coalesced loads)
+        const int t = w0 + i;
+        const int at = (i % kRowT) * kRowPad + i / kRowT;
+        if (t < g.U) {
+          const uint32_t nr = C[rk + t];
+          const uint64_t SH = Hnb + Sh[rk + t];
+          const uint32_t nH = (n - Rk) + nr;
+          s_nH[at] = (double)nH;
+          s_SHs[at] = __dmul_rn((double)SH, inv);
+          s_LP[at] = light_part(bl, pl, (double)(n - nH), __dmul_rn((double)(Htot - SH), inv));
+          s_cls[at] = t == 0 || nr != C[rk + t - 1];
+        } else {                                         // past the row end: S = +inf
+          s_nH[at] = 0.0;
+          s_SHs[at] = 0.0;
+          s_LP[at] = INFINITY;
+          s_cls[at] = 2;
+        }
+      }
+      __syncwarp();
+      for (int p = q0; p < q1; ++p) {
+        const PairConst& pc = sm.pc[p - p0];
+        const double ph = pc.ph, bh = pc.bh;
+        unsigned long long key[kRowT];
+        unsigned long long lmin = ~0ull;
+#pragma unroll
+        for (int j = 0; j < kRowT; ++j) {
+          const int at = j * kRowPad + lane;
+          key[j] = order_key_fast(fid_num(bh, ph, s_nH[at], s_SHs[at], s_LP[at]));
+          lmin = min(lmin, key[j]);
+        }
+        unsigned long long incl = lmin;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl = min(incl, o);
+        }
+        unsigned long long run = __shfl_up_sync(0xffffffffu, incl, 1);
+        const unsigned long long carry = sm.carry[warp][p - q0];
+        run = lane == 0 ? carry : min(carry, run);
+        const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        if (lane == 0) sm.carry[warp][p - q0] = min(carry, tot);
+        unsigned take = 0;
+        const double dpc = pc.delta2_S;
+#pragma unroll
+        for (int j = 0; j < kRowT; ++j) {
+          bool t_ok;
+          if (kFilter) {
+            const double rowmin = run == ~0ull ? INFINITY : from_order_key(run);
+            t_ok = s_cls[j * kRowPad + lane] == 1 && from_order_key(key[j]) <= rowmin + dpc;
+          } else {
+            t_ok = key[j] < run;
+          }
+          take |= (unsigned)t_ok << j;
+          run = min(run, key[j]);
+        }
+        visit(p, pc, w0, key, take);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// F1: per (pair, latency bucket) minimum of S over the row-frontier cells --
+// enough for the EXCLUSIVE bucket prefix minima (a cell dropped here is
+// dominated by an earlier cell of its row, which sits in the same or a lower
+// bucket).  Reads the current minima first (all in flight): most cells do
+// not lower them.
+__global__ void __launch_bounds__(kRowWarps * 32)
 bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
                   const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
-  const int grp = blockIdx.y;
-  if (grp >= *n_groups) return;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)g.U * g.U) return;
-  const int k = (int)(c / g.U), t = (int)(c % g.U);
-  const int p0 = group_p0[grp], p1 = group_p0[grp + 1];
-  const int slot = pcs[p0].slot;
-  const uint32_t* C = slot_cnt(g, slot);
-  if (!class_start(g, C, k, t)) return;   // exact duplicate of an earlier cell
-  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
-  for (int p = p0; p < p1; ++p) {
-    const PairConst pc = pcs[p];
-    double x, S;
-    numerators_of(g, pc, ci, &x, &S);
-    const int b = bucket_of_x(pc, g.nbuckets, x);
-    atomicMin(&bmin[(int64_t)p * g.nbuckets + b], (unsigned long long)order_key(S));
-  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  int p0, p1, k;
+  if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k)) return;
+  const int lane = threadIdx.x & 31;
+  const double dRk = (double)slot_cnt(g, sm.pc[0].slot)[(int64_t)k * g.B1 + g.U];
+  const double* s_nH = sm.nH[threadIdx.x >> 5];
+  row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
+                                            const unsigned long long* key, unsigned take) {
+    unsigned long long* const bp = bmin + (int64_t)p * g.nbuckets;
+    const double xr = __dmul_rn(dRk, pc.Ll);
+    int bk[kRowT];
+    unsigned long long cur[kRowT];
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j)
+      bk[j] = bucket_of_x(pc, g.nbuckets, __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)));
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j) cur[j] = (take >> j & 1u) ? bp[bk[j]] : 0ull;
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j)
+      if (key[j] < cur[j]) atomicMin(bp + bk[j], key[j]);
+  });
 }
 
 // ------------------------------------------------- F2: exclusive prefix minima
@@ -395,14 +561,6 @@ prefix_apply_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
 }
 
 // ------------------------------------------------------------- F3: filter
-
-struct Cands {
-  uint32_t* pair;
-  uint32_t* cell;     // k * U + t
-  uint32_t* bucket;
-  double* lat;
-  double* fid;
-};
 
 // ---------------------------------------------- F4: offsets (exclusive scan)
 
@@ -565,14 +723,16 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
   }
   for (int64_t j = s0; j < s1 && !killed; ++j) {
     if (j == self) continue;
-    const double ld = grp.lat[j];
+    const double ld = grp.c[j].lat;
     if (ld > lat) continue;
-    const double fd = grp.fid[j];
-    const uint32_t dc = grp.cell[j];
-    const int kd = (int)(dc / g.U), td = (int)(dc % g.U);
+    const double fd = grp.c[j].fid;
     if (fabs(fd - fid) > pc.delta2) {
       if (fd < fid) killed = true;
-    } else if (same_heavy(g, pc.slot, kd, td, k, t)) {
+      continue;
+    }
+    const uint32_t dc = grp.c[j].cell;
+    const int kd = (int)(dc / g.U), td = (int)(dc % g.U);
+    if (same_heavy(g, pc.slot, kd, td, k, t)) {
       if (ld < lat || grid_index(g, kd, td) < idx) killed = true;
     } else {
       unsure = true;
@@ -588,47 +748,82 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
   }
 }
 
-// Two passes over the cells: COUNT candidates per (pair, bucket), scan the
-// counts into bucket offsets, then WRITE every candidate straight into its
-// bucket's segment -- no global candidate counter, no separate scatter.
-template <bool kWrite>
-__global__ void __launch_bounds__(kCellThreads)
+// F3: candidates = class-start cells within 2 delta (numerator space) of both
+// their row's prefix minimum and their bucket's exclusive prefix minimum.
+// They are appended to an unordered list (one atomic per warp and partner)
+// and counted per (pair, bucket); F5 then groups them by bucket.
+
+__global__ void __launch_bounds__(kRowWarps * 32)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
-              uint32_t* __restrict__ bcnt, const unsigned long long* __restrict__ boff,
-              uint32_t* __restrict__ bcur, Cands grp, int64_t cap, DecideOut o) {
-  const int gi = blockIdx.y;
-  if (gi >= *n_groups) return;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)g.U * g.U) return;
-  const int k = (int)(c / g.U), t = (int)(c % g.U);
-  const int p0 = group_p0[gi], p1 = group_p0[gi + 1];
-  const int slot = pcs[p0].slot;
-  const uint32_t* C = slot_cnt(g, slot);
-  if (!class_start(g, C, k, t)) return;
-  const CellInts ci = cell_ints(g, C, slot_hs(g, slot), k, t);
-  const double dn = (double)g.n;
-  uint32_t rep = 0xffffffffu;
-  for (int p = p0; p < p1; ++p) {
-    const PairConst pc = pcs[p];
-    double x, S;
-    numerators_of(g, pc, ci, &x, &S);
-    const int b = bucket_of_x(pc, g.nbuckets, x);
-    const int64_t key = (int64_t)p * g.nbuckets + b;
-    if (!(S <= gpre[key] + pc.delta2_S)) continue;
-    if (!kWrite) {
-      atomicAdd(&bcnt[key], 1u);
-      continue;
+              uint32_t* __restrict__ bcnt, Cands lst, int64_t cap,
+              unsigned long long* __restrict__ n_list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  int p0, p1, k;
+  if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k)) return;
+  const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
+  const int lane = threadIdx.x & 31;
+  const uint32_t krep = (uint32_t)g.row_rep[k] * (uint32_t)g.U;
+  const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
+  const double* s_nH = sm.nH[threadIdx.x >> 5];
+  row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
+                                           const unsigned long long* key, unsigned take) {
+    const double* const gp = gpre + (int64_t)p * g.nbuckets;
+    const double xr = __dmul_rn(dRk, pc.Ll);
+    int bk[kRowT];
+    double gv[kRowT];
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j)
+      bk[j] = bucket_of_x(pc, g.nbuckets, __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)));
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j]] : -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j)
+      if (!(from_order_key(key[j]) <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
+    // one list reservation per (window, partner)
+    const int cnt = __popc(take);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
     }
-    const int64_t at = (int64_t)boff[key] + atomicAdd(&bcur[key], 1u);
-    if (at >= cap) continue;
-    if (rep == 0xffffffffu) rep = rep_cell(g, C, k, t, true);
-    const double lat = __ddiv_rn(x, dn), fid = __ddiv_rn(S, dn);
-    grp.pair[at] = (uint32_t)p;
-    grp.cell[at] = rep;
-    grp.bucket[at] = (uint32_t)b;
-    grp.lat[at] = lat;
-    grp.fid[at] = fid;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    unsigned long long at0 = 0;
+    if (lane == 31) at0 = atomicAdd(n_list, (unsigned long long)total);
+    int64_t at = (int64_t)__shfl_sync(0xffffffffu, at0, 31) + incl - cnt;
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j) {
+      if (!(take >> j & 1u)) continue;
+      atomicAdd(&bcnt[(int64_t)p * g.nbuckets + bk[j]], 1u);
+      if (at < cap) {
+        // raw numerators; F5 divides (lat = x / n, fid* = S / n)
+        const int t = w0 + lane * kRowT + j;
+        lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)rep_tau(g, C, k, t, true), (uint32_t)bk[j], 0u,
+                         __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)),
+                         from_order_key(key[j])};
+      }
+      ++at;
+    }
+  });
+}
+
+// F5: group the candidate list by (pair, bucket) with the scanned counts
+__global__ void group_cands_kernel(Cands lst, const unsigned long long* __restrict__ n_list,
+                                   int64_t cap, int nbuckets, double dn,
+                                   const unsigned long long* __restrict__ boff,
+                                   uint32_t* __restrict__ bcur, Cands grp) {
+  if ((int64_t)*n_list > cap) return;
+  const int64_t m = (int64_t)*n_list;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    Cand cd = lst.c[i];
+    cd.lat = __ddiv_rn(cd.lat, dn);       // the list holds raw numerators
+    cd.fid = __ddiv_rn(cd.fid, dn);
+    const int64_t key = (int64_t)cd.pair * nbuckets + cd.bucket;
+    grp.c[(int64_t)boff[key] + atomicAdd(&bcur[key], 1u)] = cd;
   }
 }
 
@@ -647,10 +842,10 @@ __global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
   const int64_t m = (int64_t)counters_ro[0];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const int p = (int)grp.pair[i];
-    const int64_t key = (int64_t)p * g.nbuckets + grp.bucket[i];
+    const int p = (int)grp.c[i].pair;
+    const int64_t key = (int64_t)p * g.nbuckets + grp.c[i].bucket;
     const int64_t s0 = (int64_t)boff[key];
-    decide_one(g, pcs[p], p, grp.cell[i], grp.lat[i], grp.fid[i], gpre[key], grp, s0,
+    decide_one(g, pcs[p], p, grp.c[i].cell, grp.c[i].lat, grp.c[i].fid, gpre[key], grp, s0,
                min(s0 + (int64_t)bcnt[key], m), i, o);
   }
 }
@@ -740,8 +935,8 @@ __global__ void partners_kernel(Grid g, const PairConst* __restrict__ pcs,
       const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
       const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
       for (int64_t j = s0 + threadIdx.x; j < s1; j += blockDim.x) {
-        if (grp.lat[j] > v.lat || fabs(grp.fid[j] - v.fid) > pc.delta2) continue;
-        request_exact(cells, p, grp.cell[j], req_bm, req_pair, req_cell, rcap, counters);
+        if (grp.c[j].lat > v.lat || fabs(grp.c[j].fid - v.fid) > pc.delta2) continue;
+        request_exact(cells, p, grp.c[j].cell, req_bm, req_pair, req_cell, rcap, counters);
       }
     } else {
       const uint32_t* C = slot_cnt(g, pc.slot);
@@ -903,11 +1098,11 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
       const int64_t s0 = (int64_t)boff[(int64_t)p * g.nbuckets];
       const int64_t s1 = min((int64_t)boff[(int64_t)p * g.nbuckets + b + 1], m);
       for (int64_t j = s0 + threadIdx.x; j < s1 && have_c; j += blockDim.x) {
-        const uint32_t dc = grp.cell[j];
+        const uint32_t dc = grp.c[j].cell;
         if (dc == cell) continue;
-        const double ld = grp.lat[j];
+        const double ld = grp.c[j].lat;
         if (ld > v.lat) continue;
-        double fd = grp.fid[j];
+        double fd = grp.c[j].fid;
         double fcc = v.fid;
         if (fabs(fd - v.fid) <= pc.delta2) {
           if (!lookup_exact(nr, cells, req_pair, req_cell, req_fid, p, dc, &fd)) { atomicMax(&s_kill, 2); continue; }
@@ -1087,7 +1282,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, grp[5], kept, reqbm, un[3], req[3],
+  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
       counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
@@ -1112,8 +1307,8 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.bcnt = take(4 * pb);
   L.bcur = take(4 * pb);
   L.boff = take(8 * (pb + 1));
-  L.grp[0] = take(4 * cap); L.grp[1] = take(4 * cap); L.grp[2] = take(4 * cap);
-  L.grp[3] = take(8 * cap); L.grp[4] = take(8 * cap);
+  L.grp = take(sizeof(Cand) * cap);
+  L.lst = take(sizeof(Cand) * cap);
   L.kept = take(4 * words);
   L.reqbm = take(4 * words);
   L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
@@ -1134,10 +1329,13 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   return L;
 }
 
+// Latency buckets per pair: coarse enough that the bucket minima stay
+// L2-resident (2^16 x 8 B per pair); candidates are pre-thinned by the row
+// prefix-min, so coarse buckets admit few extra candidates.
 static int buckets_for(int U) {
   const int64_t cells = (int64_t)U * U;
   int64_t b = 1024;
-  while (b < cells / 4 && b < (1 << 18)) b <<= 1;
+  while (b < cells / 16 && b < (1 << 16)) b <<= 1;
   return (int)b;
 }
 
@@ -1187,8 +1385,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* bcnt = (uint32_t*)P(L.bcnt);
   uint32_t* bcur = (uint32_t*)P(L.bcur);
   unsigned long long* boff = (unsigned long long*)P(L.boff);
-  Cands grp{(uint32_t*)P(L.grp[0]), (uint32_t*)P(L.grp[1]), (uint32_t*)P(L.grp[2]),
-            (double*)P(L.grp[3]), (double*)P(L.grp[4])};
+  Cands grp{(Cand*)P(L.grp)};
+  Cands lst{(Cand*)P(L.lst)};
   uint32_t* kept = (uint32_t*)P(L.kept);
   uint32_t* reqbm = (uint32_t*)P(L.reqbm);
   Uncertain un{(uint32_t*)P(L.un[0]), (uint32_t*)P(L.un[1]), (uint32_t*)P(L.un[2])};
@@ -1227,12 +1425,14 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
                                                             sorted);
   HADIS_LAUNCH_CHECK();
 
-  const int64_t total_cells = cells * n_pairs;
-  int64_t grid_cells = ceil_div(total_cells, kCellThreads);
-  if (grid_cells > (int64_t)kNumSMs * 16) grid_cells = (int64_t)kNumSMs * 16;
-  const dim3 cell_grid((unsigned)ceil_div(cells, kCellThreads), (unsigned)n_pairs);
-  group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups);
-  bucket_min_kernel<<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, bmin);
+  const dim3 row_grid((unsigned)ceil_div(n_unique, kRowWarps), (unsigned)n_pairs);
+  group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups, counters, kMaxGroup);
+  const size_t rsm = sizeof(RowSmem);
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_min_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(filter_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+  bucket_min_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, bmin);
   {
     const int tiles = (int)ceil_div(nb, kPrefTile);
     prefix_tile_min_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin);
@@ -1240,8 +1440,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
     prefix_apply_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin, gpre);
   }
   const DecideOut dout{kept, un, exact_cap, reqbm, req_pair, req_cell, exact_cap, counters};
-  filter_kernel<false><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
-                                                          boff, bcur, grp, cand_cap, dout);
+  filter_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt, lst,
+                                                     cand_cap, counters + 5);
   {
     const int64_t tiles = ceil_div(pb, kScanTile);
     tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum);
@@ -1249,8 +1449,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
     tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
-  filter_kernel<true><<<cell_grid, kCellThreads, 0, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt,
-                                                         boff, bcur, grp, cand_cap, dout);
+  group_cands_kernel<<<kNumSMs * 8, 256, 0, st>>>(lst, counters + 5, cand_cap, nb, (double)n, boff,
+                                                  bcur,
+                                                  grp);
   HADIS_LAUNCH_CHECK();
   decide_kernel<<<kNumSMs * 8, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);

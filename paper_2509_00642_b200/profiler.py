@@ -392,6 +392,9 @@ class GridProfiler:
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW] == 0:
                 break
+            if stats[_lib.ST_OVERFLOW] & 128:
+                raise ProfileError("profile_records: more than 65 pool models per light stage "
+                                   "is not supported")
             if stats[_lib.ST_OVERFLOW] & (2 | 4 | 64):
                 raise ProfileError("profile_records: too many exactness-critical cells "
                                    f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
