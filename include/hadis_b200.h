@@ -80,13 +80,16 @@ int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_l
  * global atomics.  One pass reads h and the n_light score rows (row stride n)
  * once and writes, row-bucketed (rows in bh order, order within a row
  * unspecified):
- *   hfix_rows[i]       = floor(h * 2^hfix_shift)          (uint64[n])
- *   bs_rows[l][i]      = #{u <= s_l}  (the tau-bin)        (uint16[n_light][n])
+ *   hfix_rows[i]            = floor(h * 2^hfix_shift)      (uint64[n])
+ *   bs_rows[l/4][i][l%4]    = #{u <= s_l}  (the tau-bin)    (uint16, model quads)
+ * bs_rows holds hadis_bs_store_elems(n, n_light) uint16 (light models padded
+ * to a multiple of 4): one 8-byte word per record and quad of models.
  * row_plan (hadis_row_plan_bytes) receives the row offsets and K1's work
  * items; pass it unchanged to hadis_bin_hist_rows.  bad_records (device
  * uint32, may be NULL) counts hardness values that are NaN or outside [0, 1].
  * Supports up to 2047 distinct thresholds (hadis_bin_hist covers larger). */
 size_t hadis_row_plan_bytes(int32_t n_unique);
+int64_t hadis_bs_store_elems(int64_t n, int32_t n_light);
 int hadis_records_bucket(const double* h, const double* scores, int64_t n, int32_t n_light,
                          const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
                          uint64_t* hfix_rows, uint16_t* bs_rows, uint32_t* bad_records,

@@ -34,6 +34,7 @@ _SIGNATURES = {
                                 _c_vp, _c_vp]),
     "hadis_hist_scan": (_c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp]),
     "hadis_row_plan_bytes": (_c_sz, [_c_i32]),
+    "hadis_bs_store_elems": (_c_i64, [_c_i64, _c_i32]),
     "hadis_records_bucket": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
                                       _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_bin_hist_rows": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp,

@@ -119,36 +119,66 @@ __global__ void scan_rows_kernel(uint32_t* __restrict__ cnt, unsigned long long*
   }
 }
 
-// K2b: inclusive prefix along bh: one thread per (light slot, column),
-// coalesced across columns, rows walked in order.
-__global__ void scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs,
-                                 int n_light, int B1) {
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= (int64_t)n_light * B1) return;
-  const int64_t l = col / B1, t = col % B1;
-  uint32_t* c = cnt + l * B1 * B1 + t;
-  unsigned long long* s = hs + l * B1 * B1 + t;
-  uint32_t acc_c = 0;
-  unsigned long long acc_s = 0;
-  int k = 0;
-  for (; k + 8 <= B1; k += 8) {       // 8 independent loads in flight per thread
-    uint32_t vc[8];
-    unsigned long long vs[8];
+// K2b: inclusive prefix along bh.  CTA = (32-column tile, light slot); each
+// of the 16 warps takes a contiguous band of rows (lanes = columns, so every
+// access is a coalesced 128/256-byte row segment), sums its band, the bands'
+// totals are scanned in shared memory, then each warp rewrites its band with
+// the carried-in prefix (the second read hits L2).
+constexpr int kColWarps = 16;
+
+__global__ void __launch_bounds__(kColWarps * 32)
+scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs, int n_light,
+                 int B1) {
+  __shared__ uint32_t s_c[kColWarps][32];
+  __shared__ unsigned long long s_h[kColWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int64_t l = blockIdx.y;
+  const int band = (B1 + kColWarps - 1) / kColWarps;
+  const int k0 = warp * band, k1 = min(B1, k0 + band);
+  uint32_t* c = cnt + l * B1 * (int64_t)B1 + t;
+  unsigned long long* h = hs + l * B1 * (int64_t)B1 + t;
+  const bool col = t < B1;
+  uint32_t sc = 0;
+  unsigned long long sh = 0;
+  if (col) {
+    int k = k0;
+    for (; k + 4 <= k1; k += 4) {
+      uint32_t vc[4];
+      unsigned long long vh[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vs[j] = s[(int64_t)(k + j) * B1]; }
+      for (int j = 0; j < 4; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      acc_c += vc[j];
-      acc_s += vs[j];
-      c[(int64_t)(k + j) * B1] = acc_c;
-      s[(int64_t)(k + j) * B1] = acc_s;
+      for (int j = 0; j < 4; ++j) { sc += vc[j]; sh += vh[j]; }
+    }
+    for (; k < k1; ++k) { sc += c[(int64_t)k * B1]; sh += h[(int64_t)k * B1]; }
+  }
+  s_c[warp][lane] = sc;
+  s_h[warp][lane] = sh;
+  __syncthreads();
+  uint32_t rc = 0;
+  unsigned long long rh = 0;
+  for (int w = 0; w < warp; ++w) { rc += s_c[w][lane]; rh += s_h[w][lane]; }
+  if (!col) return;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    uint32_t vc[4];
+    unsigned long long vh[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      rc += vc[j];
+      rh += vh[j];
+      c[(int64_t)(k + j) * B1] = rc;
+      h[(int64_t)(k + j) * B1] = rh;
     }
   }
-  for (; k < B1; ++k) {
-    acc_c += c[(int64_t)k * B1];
-    acc_s += s[(int64_t)k * B1];
-    c[(int64_t)k * B1] = acc_c;
-    s[(int64_t)k * B1] = acc_s;
+  for (; k < k1; ++k) {
+    rc += c[(int64_t)k * B1];
+    rh += h[(int64_t)k * B1];
+    c[(int64_t)k * B1] = rc;
+    h[(int64_t)k * B1] = rh;
   }
 }
 
@@ -214,8 +244,7 @@ extern "C" int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t 
   scan_rows_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(
       hist_cnt, (unsigned long long*)hist_hsum, rows, B1, row_scanned);
   HADIS_LAUNCH_CHECK();
-  const int64_t cols = (int64_t)n_light * B1;
-  scan_cols_kernel<<<(unsigned)ceil_div(cols, 128), 128, 0, st>>>(
+  scan_cols_kernel<<<dim3((unsigned)ceil_div(B1, 32), (unsigned)n_light), kColWarps * 32, 0, st>>>(
       hist_cnt, (unsigned long long*)hist_hsum, n_light, B1);
   HADIS_LAUNCH_CHECK();
   hadis_count_launches(2);

@@ -17,13 +17,13 @@
 //             memory (ATOMS ranks + one global cursor reservation per row),
 //             then written row-bucketed and staged so consecutive threads
 //             store consecutive addresses: hfix = floor(h * 2^shift) as u64
-//             and, per light model, the tau-bin bs as u16 (the score itself
-//             is never needed again).  Order within a row is irrelevant:
-//             every K1 sum is an integer sum.
-// K1 row_hist one CTA per (row chunk, light model) accumulates the row's
-//             bs-histogram (count + 16-bit hardness limbs relative to the
+//             and the tau-bins bs (u16) of four light models per 8-byte
+//             store (the scores themselves are never needed again).  Order
+//             within a row is irrelevant: every K1 sum is an integer sum.
+// K1 row_hist one CTA per (row chunk, model quad) accumulates the row's four
+//             bs-histograms (count + 16-bit hardness limbs relative to the
 //             row's fixed-point lower bound) with shared-memory ATOMS and
-//             stores the row, already prefix-summed along bs when it owns
+//             stores the rows, already prefix-summed along bs when it owns
 //             the whole row (K2's row pass fused).
 // The original-order arrays stay with the caller for the numpy-exact
 // fidelity emulation, which depends on the reference's summation order.
@@ -53,9 +53,15 @@ struct RowPlan {
   uint32_t* guide_lt;    // [kGuide + 1]
   uint32_t* guide_le;    // [kGuide + 1]
   uint32_t* bad;         // [1]
+  uint32_t* sparse;      // [1] nonzero: some guide bucket holds > 2 thresholds
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// tau-bin store: light models in quads, bs[quad][record][4] (uint16), so one
+// 8-byte store / load moves a record's bins of four models
+constexpr int kQuad = 4;
+__host__ __device__ inline int64_t n_quads(int n_light) { return (n_light + kQuad - 1) / kQuad; }
 
 __host__ __device__ inline RowPlan row_plan_at(void* base) {
   unsigned char* p = (unsigned char*)base;
@@ -70,17 +76,34 @@ __host__ __device__ inline RowPlan row_plan_at(void* base) {
   r.guide_lt = (uint32_t*)(p + o);    o += align256(4 * (kGuide + 1));
   r.guide_le = (uint32_t*)(p + o);    o += align256(4 * (kGuide + 1));
   r.bad = (uint32_t*)(p + o);         o += align256(4);
+  r.sparse = (uint32_t*)(p + o);      o += align256(4);
   return r;
 }
 
 static size_t row_plan_size() {
   return align256(4 * kMaxBins) * 2 + align256(8 * (kMaxBins + 1)) * 2 + align256(8 * kMaxBins) +
-         align256(kMaxBins) + align256(4 * (kGuide + 1)) * 2 + align256(4);
+         align256(kMaxBins) + align256(4 * (kGuide + 1)) * 2 + align256(4) * 2;
 }
 
 // #{u < x} (kLE = false) or #{u <= x} (kLE = true) over sorted unique u, with
 // a guide table g(j) = #{u op j/G} packed as (g(j), g(j+1)): for x in
 // [j/G, (j+1)/G) the answer lies in [g(j), g(j+1)].  x*G is exact (G = 2^12).
+template <bool kLE>
+__device__ __forceinline__ int guided_bin(const double* u, int U, const uint32_t* guide, double x);
+
+// Branch-free variant when every guide bucket holds at most two thresholds
+// (rp.sparse == 0): u must be padded with two +inf entries (u[U], u[U+1]).
+template <bool kLE>
+__device__ __forceinline__ int guided_bin_dense(const double* u, int U, const uint32_t* guide,
+                                                double x) {
+  if (x >= 0.0 && x <= 1.0) {
+    const int b = (int)(guide[__double2int_rz(x * kGuide)] & 0xffffu);
+    const double u0 = u[b], u1 = u[b + 1];
+    return b + (kLE ? (u0 <= x) + (u1 <= x) : (u0 < x) + (u1 < x));
+  }
+  return kLE ? count_less_equal(u, U, x) : count_less(u, U, x);
+}
+
 template <bool kLE>
 __device__ __forceinline__ int guided_bin(const double* u, int U, const uint32_t* guide, double x) {
   if (x >= 0.0 && x <= 1.0) {
@@ -104,7 +127,6 @@ __device__ __forceinline__ int guided_bin(const double* u, int U, const uint32_t
 __global__ void bucket_setup_kernel(const double* __restrict__ thr, int U, RowPlan rp) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < kMaxBins) rp.row_cnt[j] = 0;
-  if (j == 0) *rp.bad = 0;
   if (j > kGuide + 1) return;
   auto cnt = [&](double x, bool le) {
     int lo = 0, hi = U;
@@ -117,8 +139,10 @@ __global__ void bucket_setup_kernel(const double* __restrict__ thr, int U, RowPl
   if (j <= kGuide) {
     const double x0 = (double)j / kGuide;
     const double x1 = (double)(j < kGuide ? j + 1 : kGuide) / kGuide;
-    rp.guide_lt[j] = (uint32_t)cnt(x0, false) | ((uint32_t)cnt(x1, false) << 16);
-    rp.guide_le[j] = (uint32_t)cnt(x0, true) | ((uint32_t)cnt(x1, true) << 16);
+    const int a0 = cnt(x0, false), a1 = cnt(x1, false), e0 = cnt(x0, true), e1 = cnt(x1, true);
+    rp.guide_lt[j] = (uint32_t)a0 | ((uint32_t)a1 << 16);
+    rp.guide_le[j] = (uint32_t)e0 | ((uint32_t)e1 << 16);
+    if (a1 - a0 > 2 || e1 - e0 > 2) atomicOr(rp.sparse, 1u);
   }
 }
 
@@ -132,8 +156,9 @@ bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __res
   double* s_thr = reinterpret_cast<double*>(s_guide + kGuide + 2); // [U]
   for (int i = threadIdx.x; i <= U; i += blockDim.x) s_cnt[i] = 0;
   for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) s_guide[i] = rp.guide_lt[i];
-  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+  for (int i = threadIdx.x; i < U + 2; i += blockDim.x) s_thr[i] = i < U ? thr[i] : INFINITY;
   __syncthreads();
+  const bool dense = *rp.sparse == 0;
   uint32_t my_bad = 0;
   const int64_t n2 = n >> 1;
   const double2* h2 = reinterpret_cast<const double2*>(h);
@@ -141,7 +166,8 @@ bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __res
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   auto one = [&](double x) {
     my_bad += !(x >= 0.0 && x <= 1.0);
-    atomicAdd(&s_cnt[guided_bin<false>(s_thr, U, s_guide, x)], 1u);
+    atomicAdd(&s_cnt[dense ? guided_bin_dense<false>(s_thr, U, s_guide, x)
+                           : guided_bin<false>(s_thr, U, s_guide, x)], 1u);
   };
   if (vec) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
@@ -220,6 +246,18 @@ bucket_plan_kernel(const double* __restrict__ thr, int U, double hscale, RowPlan
   if (threadIdx.x == 0) { rp.row_off[U + 1] = s_carry[0]; rp.item_off[U + 1] = s_carry[1]; }
 }
 
+// Stage write-out: slot i -> its global position.  kBkPer slots per thread
+// per pass, unrolled so the shared-memory reads of a pass are all in flight.
+template <typename F>
+__device__ __forceinline__ void write_out(int cnt, F&& store) {
+  if (cnt == kBkTile) {
+#pragma unroll
+    for (int e = 0; e < kBkPer; ++e) store(e * kBkThreads + threadIdx.x);
+  } else {
+    for (int i = threadIdx.x; i < cnt; i += kBkThreads) store(i);
+  }
+}
+
 // B3: scatter.  Tile t covers records [t*kBkTile, (t+1)*kBkTile); thread i
 // owns records tile0 + 2*(j*kBkThreads + i) + {0, 1}, j < kBkPer/2, so each
 // warp load is one 512-byte 128-bit-per-lane transaction.
@@ -227,11 +265,12 @@ template <bool kVec>
 __global__ void __launch_bounds__(kBkThreads, 2)
 bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
                       int n_light, const double* __restrict__ thr, int U, double hscale,
-                      RowPlan rp, uint32_t* __restrict__ hfix_rows, uint16_t* __restrict__ bs_rows) {
+                      RowPlan rp, uint64_t* __restrict__ hfix_rows, uint16_t* __restrict__ bs_rows) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_gpos = reinterpret_cast<uint32_t*>(smem);       // [kBkTile] sorted -> global pos
-  uint32_t* s_stage = s_gpos + kBkTile;                        // [kBkTile]
-  uint32_t* s_cnt = s_stage + kBkTile;                         // [kMaxBins]
+  unsigned long long* s_st64 = reinterpret_cast<unsigned long long*>(smem);  // [kBkTile]
+  uint16_t* s_st16 = reinterpret_cast<uint16_t*>(s_st64);                   // [kQuad][kBkTile]
+  uint32_t* s_gpos = reinterpret_cast<uint32_t*>(s_st64 + kBkTile);  // [kBkTile] sorted -> global
+  uint32_t* s_cnt = s_gpos + kBkTile;                          // [kMaxBins]
   uint32_t* s_gbase = s_cnt + kMaxBins;                        // [kMaxBins]
   uint32_t* s_guide_lt = s_gbase + kMaxBins;                   // [kGuide + 1]
   uint32_t* s_guide_le = s_guide_lt + (kGuide + 2);            // [kGuide + 1]
@@ -242,9 +281,10 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
     s_guide_lt[i] = rp.guide_lt[i];
     s_guide_le[i] = rp.guide_le[i];
   }
-  for (int i = threadIdx.x; i < U; i += blockDim.x) s_thr[i] = thr[i];
+  for (int i = threadIdx.x; i < U + 2; i += blockDim.x) s_thr[i] = i < U ? thr[i] : INFINITY;
   const int B1 = U + 1;
   const int64_t tiles = ceil_div(n, kBkTile);
+  const bool dense = *rp.sparse == 0;
   constexpr int kP = kBkPer / 2;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kBkTile;
@@ -270,7 +310,8 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
       for (int e = 0; e < 2; ++e) {
         if (r + e < tn) {
           const double x = xs[e];
-          const int b = guided_bin<false>(s_thr, U, s_guide_lt, x);
+          const int b = dense ? guided_bin_dense<false>(s_thr, U, s_guide_lt, x)
+                              : guided_bin<false>(s_thr, U, s_guide_lt, x);
           const uint32_t rank = atomicAdd(&s_cnt[b], 1u);
           key[2 * j + e] = ((uint32_t)b << 16) | rank;
           hf[2 * j + e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
@@ -305,25 +346,18 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
         const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
         const uint32_t slot = s_cnt[b] + rank;
         s_gpos[slot] = s_gbase[b] + rank;
-        s_stage[slot] = (uint32_t)hf[e];
+        s_st64[slot] = hf[e];
         key[e] = slot;
       }
     }
     __syncthreads();
     const int cnt = (int)s_tile_n;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) hfix_rows[2 * (int64_t)s_gpos[i]] = s_stage[i];
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < kBkPer; ++e)
-      if (key[e] != 0xffffffffu) s_stage[key[e]] = (uint32_t)(hf[e] >> 32);
-    __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-      hfix_rows[2 * (int64_t)s_gpos[i] + 1] = s_stage[i];
-    // 4. per light model: tau-bins, staged into row order
-    uint16_t* s_st16 = reinterpret_cast<uint16_t*>(s_stage);
-    for (int l = 0; l < n_light; ++l) {
+    write_out(cnt, [&](int i) { hfix_rows[s_gpos[i]] = s_st64[i]; });
+    // 4. per light model: tau-bins staged into row order, four models per
+    //    write-out (one 8-byte store per record and quad).  Model l+1's
+    //    scores are loaded while model l is binned (software pipelined).
+    auto load_scores = [&](int l, double* sv) {
       const double* srow = scores + (int64_t)l * n + t0;
-      double sv[kBkPer];
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
         const int r = 2 * (j * kBkThreads + threadIdx.x);
@@ -335,139 +369,203 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
           sv[2 * j + 1] = r + 1 < tn ? srow[r + 1] : 0.0;
         }
       }
-      __syncthreads();       // previous model's stage fully written out
+    };
+    double sn[kBkPer];
+    if (n_light > 0) load_scores(0, sn);
+    for (int l = 0; l < n_light; ++l) {
+      double sv[kBkPer];
 #pragma unroll
-      for (int e = 0; e < kBkPer; ++e)
-        if (key[e] != 0xffffffffu)
-          s_st16[key[e]] = (uint16_t)guided_bin<true>(s_thr, U, s_guide_le, sv[e]);
-      __syncthreads();
-      uint16_t* orow = bs_rows + (int64_t)l * n;
-      for (int i = threadIdx.x; i < cnt; i += blockDim.x) orow[s_gpos[i]] = s_st16[i];
+      for (int e = 0; e < kBkPer; ++e) sv[e] = sn[e];
+      if (l + 1 < n_light) load_scores(l + 1, sn);
+      const int qm = l % kQuad;
+      if (qm == 0) __syncthreads();      // previous quad (or hfix) fully written out
+      uint16_t* st = s_st16 + qm * kBkTile;
+      if (dense) {
+#pragma unroll
+        for (int e = 0; e < kBkPer; ++e)
+          if (key[e] != 0xffffffffu)
+            st[key[e]] = (uint16_t)guided_bin_dense<true>(s_thr, U, s_guide_le, sv[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < kBkPer; ++e)
+          if (key[e] != 0xffffffffu)
+            st[key[e]] = (uint16_t)guided_bin<true>(s_thr, U, s_guide_le, sv[e]);
+      }
+      if (qm == kQuad - 1 || l == n_light - 1) {
+        __syncthreads();
+        ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * n;
+        write_out(cnt, [&](int i) {
+          orow[s_gpos[i]] = make_ushort4(s_st16[i], qm >= 1 ? s_st16[kBkTile + i] : 0,
+                                         qm >= 2 ? s_st16[2 * kBkTile + i] : 0,
+                                         qm >= 3 ? s_st16[3 * kBkTile + i] : 0);
+        });
+      }
     }
     __syncthreads();
   }
 }
 
-// K1: grid (light slots, items).  The light models of one item are adjacent
-// CTAs, so the item's hfix run is read from HBM once and from L2 by the rest.
-constexpr int kBinStride = kMaxBins;
-
+// K1: one CTA per (row chunk, model quad).  Each record's hfix (8 B) and its
+// four tau-bins (one 8-byte load) feed the four models' shared-memory row
+// histograms: count + 16-bit hardness limbs relative to the row's fixed-point
+// lower bound (<= kRowChunk = 2^15 records per CTA, so no 32-bit limb can
+// overflow); wide rows (span >= 2^32) add a third limb.
 template <bool kNarrow>
+__device__ __forceinline__ void row_accumulate(const uint64_t* __restrict__ hf,
+                                               const ushort4* __restrict__ bq, int64_t r0,
+                                               int64_t r1, unsigned long long base, int nm,
+                                               uint32_t* s_bin, int B1s) {
+  auto add1 = [&](uint32_t* sb, unsigned long long d, int b) {
+    uint32_t* a = sb + b;
+    atomicAdd(a, 1u);
+    atomicAdd(a + B1s, (uint32_t)(d & 0xffffu));
+    atomicAdd(a + 2 * B1s, (uint32_t)((d >> 16) & 0xffffu));
+    if (!kNarrow) atomicAdd(a + 3 * B1s, (uint32_t)(d >> 32));
+  };
+  auto add = [&](unsigned long long hv, ushort4 b) {
+    const unsigned long long d = hv - base;
+    add1(s_bin, d, b.x);
+    if (nm > 1) add1(s_bin + 4 * B1s, d, b.y);
+    if (nm > 2) add1(s_bin + 8 * B1s, d, b.z);
+    if (nm > 3) add1(s_bin + 12 * B1s, d, b.w);
+  };
+  const int64_t a0 = min(r1, (r0 + 1) & ~(int64_t)1);   // even: 16-byte aligned pairs
+  const int64_t a1 = a0 + ((r1 - a0) & ~(int64_t)1);
+  if (threadIdx.x == 0 && r0 < a0) add(hf[r0], bq[r0]);
+  if (threadIdx.x == 1 && a1 < r1) add(hf[a1], bq[a1]);
+  const ulonglong2* h2 = reinterpret_cast<const ulonglong2*>(hf);
+  const uint4* b2 = reinterpret_cast<const uint4*>(bq);   // two records' quads
+  const int64_t g0 = a0 >> 1, g1 = a1 >> 1;
+  auto q4 = [](unsigned lo, unsigned hi) {
+    return make_ushort4((unsigned short)(lo & 0xffffu), (unsigned short)(lo >> 16),
+                        (unsigned short)(hi & 0xffffu), (unsigned short)(hi >> 16));
+  };
+  int64_t g = g0 + threadIdx.x;
+  for (; g + blockDim.x < g1; g += 2 * blockDim.x) {
+    const ulonglong2 hA = h2[g], hB = h2[g + blockDim.x];
+    const uint4 bA = b2[g], bB = b2[g + blockDim.x];
+    add(hA.x, q4(bA.x, bA.y));
+    add(hA.y, q4(bA.z, bA.w));
+    add(hB.x, q4(bB.x, bB.y));
+    add(hB.y, q4(bB.z, bB.w));
+  }
+  for (; g < g1; g += blockDim.x) {
+    const ulonglong2 hA = h2[g];
+    const uint4 bA = b2[g];
+    add(hA.x, q4(bA.x, bA.y));
+    add(hA.y, q4(bA.z, bA.w));
+  }
+}
+
 __global__ void __launch_bounds__(kK1Threads)
 row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs, int64_t n, int U,
-                RowPlan rp, uint32_t* __restrict__ g_cnt, unsigned long long* __restrict__ g_hsum,
-                uint8_t* __restrict__ row_scanned) {
-  __shared__ uint32_t s_bin[4 * kBinStride];
+                int n_light, RowPlan rp, uint32_t* __restrict__ g_cnt,
+                unsigned long long* __restrict__ g_hsum, uint8_t* __restrict__ row_scanned) {
+  extern __shared__ __align__(16) uint32_t s_bin[];    // [kQuad][4][B1s]
+  __shared__ uint32_t ws_c[kK1Threads / 32];
+  __shared__ unsigned long long ws_h[kK1Threads / 32];
   const int B1 = U + 1;
+  const int B1s = B1 | 1;                               // odd stride between limb arrays
   const int64_t items = rp.item_off[U + 1];
   const int64_t item = blockIdx.y;
   if (item >= items) return;
   int lo = 0, hi = U + 1;
   while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (rp.item_off[mid] <= item) lo = mid; else hi = mid - 1; }
   const int k = lo;
-  if ((rp.row_narrow[k] != 0) != kNarrow) return;
+  const bool narrow = rp.row_narrow[k] != 0;
   const int64_t chunk = item - rp.item_off[k];
   const int64_t r0 = rp.row_off[k] + chunk * kRowChunk;
   const int64_t r1 = min(rp.row_off[k + 1], r0 + kRowChunk);
   const bool whole_row = (r0 == rp.row_off[k]) && (r1 == rp.row_off[k + 1]);
-  const int l = blockIdx.x;
-  for (int i = threadIdx.x; i < (kNarrow ? 3 : 4) * kBinStride; i += blockDim.x) s_bin[i] = 0;
+  const int quad = blockIdx.x;
+  const int nm = min(kQuad, n_light - quad * kQuad);
+  for (int i = threadIdx.x; i < nm * 4 * B1s; i += blockDim.x) s_bin[i] = 0;
   __syncthreads();
-  const uint16_t* brow = bs + (int64_t)l * n;
   const unsigned long long base = rp.row_base[k];
-  auto add = [&](unsigned long long hv, int b) {
-    const unsigned long long d = hv - base;
-    uint32_t* a = s_bin + b;
-    atomicAdd(a, 1u);
-    atomicAdd(a + kBinStride, (uint32_t)(d & 0xffffu));
-    atomicAdd(a + 2 * kBinStride, (uint32_t)((d >> 16) & 0xffffu));
-    if (!kNarrow) atomicAdd(a + 3 * kBinStride, (uint32_t)(d >> 32));
-  };
-  constexpr int kU = 4;
-  int64_t q = r0 + threadIdx.x;
-  for (; q + (kU - 1) * (int64_t)blockDim.x < r1; q += kU * (int64_t)blockDim.x) {
-    unsigned long long hv[kU];
-    int bv[kU];
-#pragma unroll
-    for (int j = 0; j < kU; ++j) { hv[j] = hf[q + j * blockDim.x]; bv[j] = brow[q + j * blockDim.x]; }
-#pragma unroll
-    for (int j = 0; j < kU; ++j) add(hv[j], bv[j]);
-  }
-  for (; q < r1; q += blockDim.x) add(hf[q], brow[q]);
+  const ushort4* bq = reinterpret_cast<const ushort4*>(bs) + (int64_t)quad * n;
+  if (narrow) row_accumulate<true>(hf, bq, r0, r1, base, nm, s_bin, B1s);
+  else row_accumulate<false>(hf, bq, r0, r1, base, nm, s_bin, B1s);
   __syncthreads();
-  uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
-  unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
-  auto bin_sum = [&](int i) {
-    unsigned long long v = (unsigned long long)s_bin[i] * base + (unsigned long long)s_bin[kBinStride + i] +
-                           ((unsigned long long)s_bin[2 * kBinStride + i] << 16);
-    if (!kNarrow) v += (unsigned long long)s_bin[3 * kBinStride + i] << 32;
-    return v;
-  };
-  if (!whole_row || !row_scanned) {
-    for (int i = threadIdx.x; i < B1; i += blockDim.x) {
-      const uint32_t c = s_bin[i];
-      const unsigned long long v = bin_sum(i);
-      if (whole_row) {
-        gc[i] = c;
-        gh[i] = v;
-      } else if (c) {
-        atomicAdd(&gc[i], c);
-        atomicAdd(&gh[i], v);
+  for (int m = 0; m < nm; ++m) {
+    const int l = quad * kQuad + m;
+    const uint32_t* sb = s_bin + m * 4 * B1s;
+    uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
+    unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
+    auto bin_sum = [&](int i) {
+      return (unsigned long long)sb[i] * base + (unsigned long long)sb[B1s + i] +
+             ((unsigned long long)sb[2 * B1s + i] << 16) +
+             (narrow ? 0ull : (unsigned long long)sb[3 * B1s + i] << 32);
+    };
+    if (!whole_row || !row_scanned) {
+      for (int i = threadIdx.x; i < B1; i += blockDim.x) {
+        const uint32_t c = sb[i];
+        const unsigned long long v = bin_sum(i);
+        if (whole_row) {
+          gc[i] = c;
+          gh[i] = v;
+        } else if (c) {
+          atomicAdd(&gc[i], c);
+          atomicAdd(&gh[i], v);
+        }
       }
+      continue;
     }
-    return;
-  }
-  // whole row: emit the K2 row prefix (along bs) directly -- thread-contiguous
-  // segments, block scan of the segment totals, then the segment prefixes
-  __shared__ uint32_t ws_c[kK1Threads / 32];
-  __shared__ unsigned long long ws_h[kK1Threads / 32];
-  const int per = (B1 + blockDim.x - 1) / blockDim.x;
-  const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
-  uint32_t tc = 0;
-  unsigned long long th = 0;
-  for (int i = i0; i < i1; ++i) { tc += s_bin[i]; th += bin_sum(i); }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t ic = tc;
-  unsigned long long ih = th;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, off);
-    const unsigned long long oh = __shfl_up_sync(0xffffffffu, ih, off);
-    if (lane >= off) { ic += oc; ih += oh; }
-  }
-  if (lane == 31) { ws_c[warp] = ic; ws_h[warp] = ih; }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    uint32_t wc = lane < nw ? ws_c[lane] : 0u;
-    unsigned long long wh = lane < nw ? ws_h[lane] : 0ull;
+    // whole row: emit the K2 row prefix (along bs) directly -- thread-contiguous
+    // segments, block scan of the segment totals, then the segment prefixes
+    const int per = (B1 + blockDim.x - 1) / blockDim.x;
+    const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+    uint32_t tc = 0;
+    unsigned long long th = 0;
+    for (int i = i0; i < i1; ++i) { tc += sb[i]; th += bin_sum(i); }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t ic = tc;
+    unsigned long long ih = th;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t oc = __shfl_up_sync(0xffffffffu, wc, off);
-      const unsigned long long oh = __shfl_up_sync(0xffffffffu, wh, off);
-      if (lane >= off) { wc += oc; wh += oh; }
+      const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, off);
+      const unsigned long long oh = __shfl_up_sync(0xffffffffu, ih, off);
+      if (lane >= off) { ic += oc; ih += oh; }
     }
-    if (lane < nw) { ws_c[lane] = wc; ws_h[lane] = wh; }
+    if (lane == 31) { ws_c[warp] = ic; ws_h[warp] = ih; }
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      uint32_t wc = lane < nw ? ws_c[lane] : 0u;
+      unsigned long long wh = lane < nw ? ws_h[lane] : 0ull;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t oc = __shfl_up_sync(0xffffffffu, wc, off);
+        const unsigned long long oh = __shfl_up_sync(0xffffffffu, wh, off);
+        if (lane >= off) { wc += oc; wh += oh; }
+      }
+      if (lane < nw) { ws_c[lane] = wc; ws_h[lane] = wh; }
+    }
+    __syncthreads();
+    uint32_t rc = (warp > 0 ? ws_c[warp - 1] : 0u) + ic - tc;
+    unsigned long long rh = (warp > 0 ? ws_h[warp - 1] : 0ull) + ih - th;
+    for (int i = i0; i < i1; ++i) {
+      rc += sb[i];
+      rh += bin_sum(i);
+      gc[i] = rc;
+      gh[i] = rh;
+    }
+    if (threadIdx.x == 0) row_scanned[(int64_t)l * B1 + k] = 1;
+    __syncthreads();                                   // ws_c / ws_h reuse
   }
-  __syncthreads();
-  uint32_t rc = (warp > 0 ? ws_c[warp - 1] : 0u) + ic - tc;
-  unsigned long long rh = (warp > 0 ? ws_h[warp - 1] : 0ull) + ih - th;
-  for (int i = i0; i < i1; ++i) {
-    rc += s_bin[i];
-    rh += bin_sum(i);
-    gc[i] = rc;
-    gh[i] = rh;
-  }
-  if (threadIdx.x == 0) row_scanned[(int64_t)l * B1 + k] = 1;
 }
 
 static size_t scatter_smem(int U) {
-  return (size_t)4 * (2 * kBkTile + 2 * kMaxBins + 2 * (kGuide + 2)) + (size_t)8 * U;
+  return (size_t)8 * kBkTile + (size_t)4 * (kBkTile + 2 * kMaxBins + 2 * (kGuide + 2)) +
+         (size_t)8 * (U + 2);
 }
 
 }  // namespace hadis
 
 using namespace hadis;
+
+extern "C" int64_t hadis_bs_store_elems(int64_t n, int32_t n_light) {
+  return n <= 0 || n_light <= 0 ? 0 : n_quads(n_light) * kQuad * n;
+}
 
 extern "C" size_t hadis_row_plan_bytes(int32_t n_unique) {
   if (n_unique <= 0 || n_unique + 1 > kMaxBins) return 0;
@@ -487,9 +585,10 @@ extern "C" int hadis_records_bucket(const double* h, const double* scores, int64
   cudaStream_t st = (cudaStream_t)stream;
   const RowPlan rp = row_plan_at(row_plan);
   const double hscale = ldexp(1.0, hfix_shift);
+  HADIS_CUDA_TRY(cudaMemsetAsync(rp.bad, 0, 256 * 2, st));      // bad + sparse flags
   bucket_setup_kernel<<<(unsigned)ceil_div(kGuide + 2, 256), 256, 0, st>>>(thr_unique, n_unique, rp);
   HADIS_LAUNCH_CHECK();
-  const size_t csmem = (size_t)4 * (kMaxBins + kGuide + 2) + (size_t)8 * n_unique;
+  const size_t csmem = (size_t)4 * (kMaxBins + kGuide + 2) + (size_t)8 * (n_unique + 2);
   HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_count_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
   int64_t cgrid = ceil_div(n, 2 * kCountThreads * 8);
@@ -498,15 +597,15 @@ extern "C" int hadis_records_bucket(const double* h, const double* scores, int64
   HADIS_LAUNCH_CHECK();
   bucket_plan_kernel<<<1, 1024, 0, st>>>(thr_unique, n_unique, hscale, rp);
   HADIS_LAUNCH_CHECK();
-  const size_t ssmem = scatter_smem(n_unique);
   bool vec = (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (n & 1) == 0 &&
              (n_light == 0 || (reinterpret_cast<uintptr_t>(scores) & 15) == 0);
+  const size_t ssmem = scatter_smem(n_unique);
   auto kern = vec ? bucket_scatter_kernel<true> : bucket_scatter_kernel<false>;
   HADIS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
   int64_t sgrid = ceil_div(n, kBkTile);
   if (sgrid > kNumSMs * 2) sgrid = kNumSMs * 2;
   kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
-                                                   hscale, rp, (uint32_t*)hfix_rows, bs_rows);
+                                                   hscale, rp, hfix_rows, bs_rows);
   HADIS_LAUNCH_CHECK();
   if (bad_records)
     HADIS_CUDA_TRY(cudaMemcpyAsync(bad_records, rp.bad, 4, cudaMemcpyDeviceToDevice, st));
@@ -531,12 +630,16 @@ extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
   HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
   if (row_scanned) HADIS_CUDA_TRY(cudaMemsetAsync(row_scanned, 0, (size_t)B1 * n_light, st));
-  const dim3 grid((unsigned)n_light, (unsigned)max_items);
-  row_hist_kernel<true><<<grid, kK1Threads, 0, st>>>(hfix_rows, bs_rows, n, n_unique, rp, hist_cnt,
-                                                    (unsigned long long*)hist_hsum, row_scanned);
-  row_hist_kernel<false><<<grid, kK1Threads, 0, st>>>(hfix_rows, bs_rows, n, n_unique, rp, hist_cnt,
-                                                     (unsigned long long*)hist_hsum, row_scanned);
+  const int B1s = (n_unique + 1) | 1;
+  const size_t ksmem = (size_t)kQuad * 4 * B1s * 4;
+  if (ksmem > 48 * 1024)
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem));
+  const dim3 grid((unsigned)n_quads(n_light), (unsigned)max_items);
+  row_hist_kernel<<<grid, kK1Threads, ksmem, st>>>(hfix_rows, bs_rows, n, n_unique, n_light, rp,
+                                                  hist_cnt, (unsigned long long*)hist_hsum,
+                                                  row_scanned);
   HADIS_LAUNCH_CHECK();
-  hadis_count_launches(2);
+  hadis_count_launches(1);
   return HADIS_OK;
 }

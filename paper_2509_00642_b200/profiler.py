@@ -290,13 +290,13 @@ class GridProfiler:
         self._store = None
 
     def _bucket_store(self, n_light):
-        """Row-bucketed record store buffers (hfix u64[n], bs u16[n_light][n], row plan)."""
+        """Row-bucketed record store buffers (hfix u64[n], bs u16 model quads, row plan)."""
         torch = self.torch
         st = self._store
-        if st is None or st[1].shape[0] < n_light:
+        elems = self.lib.hadis_bs_store_elems(self.n, n_light)
+        if st is None or st[1].numel() < elems:
             st = self._store = (torch.empty(self.n, dtype=torch.int64, device=self.device),
-                                torch.empty((n_light, self.n), dtype=torch.int16,
-                                            device=self.device),
+                                torch.empty(elems, dtype=torch.int16, device=self.device),
                                 torch.empty(self.lib.hadis_row_plan_bytes(1), dtype=torch.uint8,
                                             device=self.device))
         return st
