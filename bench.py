@@ -261,7 +261,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
 
     # ---- timed region: device resident records
-    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     launches0 = _lib.load().hadis_kernel_launches()
     sampler = ClockSampler(local)
     barrier()
@@ -278,7 +278,8 @@ def run_ours(args, cfg):
     def stage(a, b):
         return statistics.mean([ev[a].elapsed_time(ev[b]) for ev in kev]) if plan is not None \
             else 0.0
-    ms_b, ms_k1, ms_k2, ms_k34 = stage(0, 1), stage(1, 2), stage(2, 3), stage(3, 4)
+    ms_plan, ms_b, ms_k1, ms_k2, ms_k34 = (stage(0, 1), stage(1, 2), stage(2, 3), stage(3, 4),
+                                           stage(4, 5))
 
     # ---- e2e: host buffers, H2D + pipeline + D2H of the row arrays every step
     e2e_ms = []
@@ -326,12 +327,12 @@ def run_ours(args, cfg):
                        "parallelism": f"pair-shard x{world} + nccl all-gather" if world > 1
                        else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
             "table_build_ms": ms_max,
-            "stage_ms": {"b_bucket": ms_b, "k1_row_hist": ms_k1, "k2_scan": ms_k2,
-                         "k3_k4_frontier": ms_k34},
+            "stage_ms": {"b0_b2_row_plan": ms_plan, "b3_scatter": ms_b, "k1_row_hist": ms_k1,
+                         "k2_scan": ms_k2, "k3_k4_frontier": ms_k34},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
-                         "kernel": "B bucket pass (B0-B3 timed together; B3 scatter carries "
-                                   "the bytes), rank 0", "peak_kind": peak_kind,
+                         "kernel": "B3 bucket_scatter_kernel (row-bucketed record store), rank 0",
+                         "peak_kind": peak_kind,
                          "algorithmic_bytes": alg_bytes, "bytes_moved_by_design": moved,
                          "moved_gbs": moved / (ms_b * 1e-3) / 1e9 if ms_b > 0 else 0.0},
             "e2e": {"value": cfg.cells / (e2e_max * 1e-3), "unit": "configs/s",

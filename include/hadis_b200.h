@@ -94,6 +94,16 @@ int hadis_records_bucket(const double* h, const double* scores, int64_t n, int32
                          const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
                          uint64_t* hfix_rows, uint16_t* bs_rows, uint32_t* bad_records,
                          void* row_plan, size_t row_plan_bytes, void* stream);
+/* The same in two steps: hadis_records_plan reads h only (guides, row counts,
+ * row offsets, K1 items -> row_plan); hadis_records_scatter is the
+ * HBM-bound pass over every record array (needs the plan). */
+int hadis_records_plan(const double* h, int64_t n, const double* thr_unique, int32_t n_unique,
+                       int32_t hfix_shift, uint32_t* bad_records, void* row_plan,
+                       size_t row_plan_bytes, void* stream);
+int hadis_records_scatter(const double* h, const double* scores, int64_t n, int32_t n_light,
+                          const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
+                          uint64_t* hfix_rows, uint16_t* bs_rows, void* row_plan,
+                          size_t row_plan_bytes, void* stream);
 
 /* K1 on the row-bucketed store: the same histogram as hadis_bin_hist, one CTA
  * per (row chunk, light model) accumulating in shared memory.  Rows a CTA

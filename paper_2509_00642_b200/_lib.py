@@ -37,6 +37,10 @@ _SIGNATURES = {
     "hadis_bs_store_elems": (_c_i64, [_c_i64, _c_i32]),
     "hadis_records_bucket": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
                                       _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "hadis_records_plan": (_c_int, [_c_vp, _c_i64, _c_vp, _c_i32, _c_i32, _c_vp, _c_vp, _c_sz,
+                                    _c_vp]),
+    "hadis_records_scatter": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
+                                       _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_bin_hist_rows": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_vp, _c_vp,
                                      _c_vp, _c_vp]),
     "hadis_frontier_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i64, _c_i64, _c_i64]),

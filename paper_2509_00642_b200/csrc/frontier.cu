@@ -692,9 +692,10 @@ struct DecideOut {
 // Certified main-universe decision for candidate `self` (pair p, representative
 // cell, bucket-mates grp[s0, s1)); G_S = exclusive prefix-min numerator of its
 // bucket.  Keeps, drops or queues the cell for the exact-fidelity resolution.
+template <typename Mate>
 __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t cell, double lat,
                            double fid, double G_S, const Cands& grp, int64_t s0, int64_t s1,
-                           int64_t self, const DecideOut& o) {
+                           int64_t self, const DecideOut& o, Mate&& mate) {
   const int k = (int)(cell / g.U), t = (int)(cell % g.U);
   const int64_t idx = grid_index(g, k, t);
   bool killed = false, unsure = false;
@@ -723,9 +724,10 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
   }
   for (int64_t j = s0; j < s1 && !killed; ++j) {
     if (j == self) continue;
-    const double ld = grp.c[j].lat;
+    const double2 lf = mate(j);               // (lat, fid) of bucket-mate j
+    const double ld = lf.x;
     if (ld > lat) continue;
-    const double fd = grp.c[j].fid;
+    const double fd = lf.y;
     if (fabs(fd - fid) > pc.delta2) {
       if (fd < fid) killed = true;
       continue;
@@ -832,21 +834,53 @@ __global__ void candidates_total_kernel(const unsigned long long* __restrict__ t
   if (blockIdx.x == 0 && threadIdx.x == 0) counters[0] = *total;
 }
 
-// one thread per candidate; bucket-mates are the candidates of its segment
-__global__ void decide_kernel(Grid g, const PairConst* __restrict__ pcs,
-                              const unsigned long long* __restrict__ counters_ro, int64_t cap,
-                              const unsigned long long* __restrict__ boff,
-                              const uint32_t* __restrict__ bcnt, const double* __restrict__ gpre,
-                              Cands grp, DecideOut o) {
+// One thread per candidate; bucket-mates are the candidates of its segment.
+// A CTA owns kDecChunk consecutive (bucket-grouped) candidates and first
+// stages the (lat, fid) of every candidate in the segments they touch --
+// up to kDecWin entries -- in shared memory, so the O(m^2) mate comparisons
+// read shared memory; segments that do not fit fall back to global reads.
+constexpr int kDecThreads = 256;
+constexpr int kDecChunk = 1024;
+constexpr int kDecWin = 3072;
+
+__global__ void __launch_bounds__(kDecThreads)
+decide_kernel(Grid g, const PairConst* __restrict__ pcs,
+              const unsigned long long* __restrict__ counters_ro, int64_t cap,
+              const unsigned long long* __restrict__ boff, const uint32_t* __restrict__ bcnt,
+              const double* __restrict__ gpre, Cands grp, DecideOut o) {
+  __shared__ double2 s_lf[kDecWin];
   if ((int64_t)counters_ro[0] > cap) return;
   const int64_t m = (int64_t)counters_ro[0];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const int p = (int)grp.c[i].pair;
-    const int64_t key = (int64_t)p * g.nbuckets + grp.c[i].bucket;
-    const int64_t s0 = (int64_t)boff[key];
-    decide_one(g, pcs[p], p, grp.c[i].cell, grp.c[i].lat, grp.c[i].fid, gpre[key], grp, s0,
-               min(s0 + (int64_t)bcnt[key], m), i, o);
+  for (int64_t c0 = (int64_t)blockIdx.x * kDecChunk; c0 < m; c0 += (int64_t)gridDim.x * kDecChunk) {
+    const int64_t c1 = min(m, c0 + kDecChunk);
+    auto seg_of = [&](int64_t i, int64_t* a, int64_t* b) {
+      const int64_t key = (int64_t)grp.c[i].pair * g.nbuckets + grp.c[i].bucket;
+      *a = (int64_t)boff[key];
+      *b = min(*a + (int64_t)bcnt[key], m);
+    };
+    int64_t sa, sb, ea, eb;
+    seg_of(c0, &sa, &sb);
+    seg_of(c1 - 1, &ea, &eb);
+    const int64_t w0 = max(sa, c0 - (kDecWin - kDecChunk) / 2);
+    const int64_t w1 = min(eb, w0 + kDecWin);
+    __syncthreads();                               // previous chunk done with s_lf
+    for (int64_t j = w0 + threadIdx.x; j < w1; j += blockDim.x)
+      s_lf[j - w0] = make_double2(grp.c[j].lat, grp.c[j].fid);
+    __syncthreads();
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const Cand cd = grp.c[i];
+      const int p = (int)cd.pair;
+      const int64_t key = (int64_t)p * g.nbuckets + cd.bucket;
+      const int64_t s0 = (int64_t)boff[key];
+      const int64_t s1 = min(s0 + (int64_t)bcnt[key], m);
+      if (s0 >= w0 && s1 <= w1) {
+        decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, gpre[key], grp, s0, s1, i, o,
+                   [&](int64_t j) { return s_lf[j - w0]; });
+      } else {
+        decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, gpre[key], grp, s0, s1, i, o,
+                   [&](int64_t j) { return make_double2(grp.c[j].lat, grp.c[j].fid); });
+      }
+    }
   }
 }
 
@@ -1453,7 +1487,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
                                                   bcur,
                                                   grp);
   HADIS_LAUNCH_CHECK();
-  decide_kernel<<<kNumSMs * 8, 256, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
+  decide_kernel<<<kNumSMs * 8, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
   if (row_smem > 48 * 1024)

@@ -572,16 +572,24 @@ extern "C" size_t hadis_row_plan_bytes(int32_t n_unique) {
   return row_plan_size();
 }
 
-extern "C" int hadis_records_bucket(const double* h, const double* scores, int64_t n,
-                                    int32_t n_light, const double* thr_unique, int32_t n_unique,
-                                    int32_t hfix_shift, uint64_t* hfix_rows, uint16_t* bs_rows,
-                                    uint32_t* bad_records, void* row_plan, size_t row_plan_bytes,
-                                    void* stream) {
-  if (!h || n <= 0 || n > 0xffffffffll || n_light < 0 || (n_light > 0 && (!scores || !bs_rows)) ||
-      !thr_unique || n_unique <= 0 || !hfix_rows || !row_plan || hfix_shift < 1 || hfix_shift > 48)
+static int records_args_ok(const double* h, const double* scores, int64_t n, int32_t n_light,
+                           const double* thr_unique, int32_t n_unique, int32_t hfix_shift,
+                           const void* row_plan, size_t row_plan_bytes) {
+  if (!h || n <= 0 || n > 0xffffffffll || n_light < 0 || (n_light > 0 && !scores) ||
+      !thr_unique || n_unique <= 0 || !row_plan || hfix_shift < 1 || hfix_shift > 48)
     return HADIS_ERR_ARG;
   if (n_unique + 1 > kMaxBins) return HADIS_ERR_UNSUPPORTED;
   if (row_plan_bytes < row_plan_size()) return HADIS_ERR_CAPACITY;
+  return HADIS_OK;
+}
+
+// B0..B2: guides, row counts, row offsets / K1 items (reads h only)
+extern "C" int hadis_records_plan(const double* h, int64_t n, const double* thr_unique,
+                                  int32_t n_unique, int32_t hfix_shift, uint32_t* bad_records,
+                                  void* row_plan, size_t row_plan_bytes, void* stream) {
+  const int rc = records_args_ok(h, h, n, 0, thr_unique, n_unique, hfix_shift, row_plan,
+                                 row_plan_bytes);
+  if (rc != HADIS_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const RowPlan rp = row_plan_at(row_plan);
   const double hscale = ldexp(1.0, hfix_shift);
@@ -597,6 +605,24 @@ extern "C" int hadis_records_bucket(const double* h, const double* scores, int64
   HADIS_LAUNCH_CHECK();
   bucket_plan_kernel<<<1, 1024, 0, st>>>(thr_unique, n_unique, hscale, rp);
   HADIS_LAUNCH_CHECK();
+  if (bad_records)
+    HADIS_CUDA_TRY(cudaMemcpyAsync(bad_records, rp.bad, 4, cudaMemcpyDeviceToDevice, st));
+  hadis_count_launches(3);
+  return HADIS_OK;
+}
+
+// B3: the HBM-bound scatter into the row-bucketed store (needs the plan)
+extern "C" int hadis_records_scatter(const double* h, const double* scores, int64_t n,
+                                     int32_t n_light, const double* thr_unique, int32_t n_unique,
+                                     int32_t hfix_shift, uint64_t* hfix_rows, uint16_t* bs_rows,
+                                     void* row_plan, size_t row_plan_bytes, void* stream) {
+  const int rc = records_args_ok(h, scores, n, n_light, thr_unique, n_unique, hfix_shift,
+                                 row_plan, row_plan_bytes);
+  if (rc != HADIS_OK) return rc;
+  if (!hfix_rows || (n_light > 0 && !bs_rows)) return HADIS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const RowPlan rp = row_plan_at(row_plan);
+  const double hscale = ldexp(1.0, hfix_shift);
   bool vec = (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (n & 1) == 0 &&
              (n_light == 0 || (reinterpret_cast<uintptr_t>(scores) & 15) == 0);
   const size_t ssmem = scatter_smem(n_unique);
@@ -607,10 +633,20 @@ extern "C" int hadis_records_bucket(const double* h, const double* scores, int64
   kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
                                                    hscale, rp, hfix_rows, bs_rows);
   HADIS_LAUNCH_CHECK();
-  if (bad_records)
-    HADIS_CUDA_TRY(cudaMemcpyAsync(bad_records, rp.bad, 4, cudaMemcpyDeviceToDevice, st));
-  hadis_count_launches(4);
+  hadis_count_launches(1);
   return HADIS_OK;
+}
+
+extern "C" int hadis_records_bucket(const double* h, const double* scores, int64_t n,
+                                    int32_t n_light, const double* thr_unique, int32_t n_unique,
+                                    int32_t hfix_shift, uint64_t* hfix_rows, uint16_t* bs_rows,
+                                    uint32_t* bad_records, void* row_plan, size_t row_plan_bytes,
+                                    void* stream) {
+  const int rc = hadis_records_plan(h, n, thr_unique, n_unique, hfix_shift, bad_records, row_plan,
+                                    row_plan_bytes, stream);
+  if (rc != HADIS_OK) return rc;
+  return hadis_records_scatter(h, scores, n, n_light, thr_unique, n_unique, hfix_shift, hfix_rows,
+                               bs_rows, row_plan, row_plan_bytes, stream);
 }
 
 extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs_rows, int64_t n,

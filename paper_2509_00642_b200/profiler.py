@@ -315,7 +315,7 @@ class GridProfiler:
     def launch(self, plan: ProfilePlan, exact_fid=False, stream=None, events=None):
         """Enqueue B (row-bucketed record store), K1 (histogram), K2 (2-D scan)
         and K3/K4 (frontier) on ``stream``; no host synchronisation.  ``events``
-        (optional list of 5 torch.cuda.Event) brackets B | K1 | K2 | K3+K4."""
+        (optional list of 6 torch.cuda.Event) brackets B0-B2 | B3 | K1 | K2 | K3+K4."""
         torch = self.torch
         dev = self.device
         st = _lib.stream_handle(stream)
@@ -331,27 +331,31 @@ class GridProfiler:
         rec(0)
         if self.layout == "bucketed" and plan.U < 2048:
             hfix, bs, rplan = self._bucket_store(plan.n_light)
-            _lib.check(self.lib.hadis_records_bucket(
-                p(self.h), p(state["scores"]), self.n, plan.n_light, p(plan.d_u), plan.U,
-                self.shift, p(hfix), p(bs), p(self.bad), p(rplan), rplan.numel(), st),
-                "hadis_records_bucket")
+            _lib.check(self.lib.hadis_records_plan(
+                p(self.h), self.n, p(plan.d_u), plan.U, self.shift, p(self.bad), p(rplan),
+                rplan.numel(), st), "hadis_records_plan")
             rec(1)
+            _lib.check(self.lib.hadis_records_scatter(
+                p(self.h), p(state["scores"]), self.n, plan.n_light, p(plan.d_u), plan.U,
+                self.shift, p(hfix), p(bs), p(rplan), rplan.numel(), st), "hadis_records_scatter")
+            rec(2)
             _lib.check(self.lib.hadis_bin_hist_rows(
                 p(hfix), p(bs), self.n, plan.n_light, plan.U, p(rplan), p(state["cnt"]),
                 p(state["hsum"]), p(state["scanned"]), st), "hadis_bin_hist_rows")
             scanned = state["scanned"]
         else:
             rec(1)
+            rec(2)
             _lib.check(self.lib.hadis_bin_hist(p(self.h), p(state["scores"]), self.n, plan.n_light,
                                                p(plan.d_u), plan.U, self.shift, p(state["cnt"]),
                                                p(state["hsum"]), p(self.bad), st), "hadis_bin_hist")
             scanned = None
-        rec(2)
+        rec(3)
         _lib.check(self.lib.hadis_hist_scan(p(state["cnt"]), p(state["hsum"]), plan.n_light,
                                             plan.U, p(scanned), st), "hadis_hist_scan")
-        rec(3)
-        self._frontier(state, plan.caps)
         rec(4)
+        self._frontier(state, plan.caps)
+        rec(5)
         return state
 
     def _frontier(self, state, caps):
