@@ -342,6 +342,7 @@ def run_ours(args, cfg):
         }
         if not args.no_allocation:
             line["allocation_search"] = measure_allocation(torch, dev, args.steps)
+            line["cascade_depth"] = measure_cascade(torch, dev, args.steps)
         traffic = _ncu_traffic(cfg.name)
         if traffic:
             line["roofline"]["traffic"] = traffic
@@ -413,6 +414,76 @@ def measure_allocation(torch, dev, steps, cpu_points=1):
             "combo_evals_per_s": P * rows * combos / (ms * 1e-3),
             "cpu_ms_per_point": cpu_ms, "cpu_points_sampled": cpu_points,
             "cpu_kind": "port", "cpu_agrees": bool(agree)}
+
+
+def measure_cascade(torch, dev, steps, n=1_000_000, k=64, models=8, cpu_points=3):
+    """every two- and three-stage cascade point of an 8-model
+    geometric catalog over a 1M-query hardness population and a 64-threshold
+    grid (hadis_cascade_points, device-resident inputs), plus the whole
+    frontier_compare (points + exact two-stage fidelities + host envelopes),
+    next to the reference's per-point numpy cost (oracle port, sampled)."""
+    from oracle import frontier as ofr
+    from paper_2509_00642_b200 import _lib, synth
+    from paper_2509_00642_b200.frontier import _accept_scores, _by_latency, frontier_compare
+    cat = synth.geometric_catalog(models)
+    vs = _by_latency(cat.variants)
+    rng = np.random.default_rng(synth.SEED)
+    h = rng.uniform(0.05, 0.9, n)
+    thr = tuple(i / (k - 1) for i in range(k))
+    lib = _lib.load()
+    M, U = len(vs), k
+    d_h = torch.from_numpy(h).to(dev)
+    d_s = torch.from_numpy(_accept_scores(vs, h)).to(dev)
+    d_p = torch.tensor([[v.latency_s[1], v.base_quality_cost, v.hardness_penalty] for v in vs],
+                       dtype=torch.float64, device=dev)
+    d_u = torch.tensor(thr, dtype=torch.float64, device=dev)
+    P2, P3 = M * (M - 1) // 2, M * (M - 1) * (M - 2) // 6
+    o2 = torch.empty(P2 * U * U * 2, dtype=torch.float64, device=dev)
+    o3 = torch.empty(P3 * U ** 3 * 2, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsb = lib.hadis_cascade_workspace_bytes(M, U)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    p = _lib.ptr
+    st = torch.cuda.current_stream()
+    shift = lib.hadis_hfix_shift(n)
+
+    def run():
+        _lib.check(lib.hadis_cascade_points(p(d_h), p(d_s), n, M, p(d_p), p(d_u), U, shift, p(o2),
+                                            p(o3), p(bad), p(ws), wsb, _lib.stream_handle(st)),
+                   "hadis_cascade_points")
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    pts = P2 * U * U + P3 * U ** 3
+    t0 = time.perf_counter()
+    rep = frontier_compare(cat, h=h, thresholds=thr)
+    compare_s = time.perf_counter() - t0
+    # reference cost per three-stage point: the oracle's numpy masks on a sample
+    hs = h
+    t0 = time.perf_counter()
+    costs, scores = ofr.model_curves(vs, hs)
+    for q in range(cpu_points):
+        theta, t1, t2 = thr[(7 * q + 11) % k], thr[(13 * q + 5) % k], thr[(3 * q + 29) % k]
+        by = hs > theta
+        keep = ~by
+        r1 = keep & (scores[0] < t1)
+        r2 = r1 & (scores[1] < t2)
+        float(costs[0][keep & ~r1].sum() + costs[1][r1 & ~r2].sum() + costs[2][by | r2].sum())
+    cpu_per_point = (time.perf_counter() - t0) / cpu_points
+    return {"workload": f"f1: {models}-model geometric catalog, {n} queries, {k} thresholds: "
+                        f"{P2 * U * U} two-stage + {P3 * U ** 3} three-stage points",
+            "points": pts, "ms_points": ms, "points_per_s": pts / (ms * 1e-3),
+            "frontier_compare_s": compare_s, "gap": rep.gap,
+            "envelope_vertices": [len(rep.envelope_two), len(rep.envelope_three)],
+            "cpu_s_per_point": cpu_per_point, "cpu_points_per_s": 1.0 / cpu_per_point,
+            "cpu_kind": "port", "cpu_points_sampled": cpu_points}
 
 
 def _ncu_traffic(name):

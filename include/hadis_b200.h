@@ -179,6 +179,27 @@ int hadis_fid_exact(const double* h, const double* scores, int64_t n, int32_t n_
                     const int32_t* cell_slot, const double* cell_theta, const double* cell_tau,
                     const double* cell_params, double* out_fid, void* stream);
 
+/* ------------------------------------------------------------------------- */
+/* Cascade-depth frontier (frontier.py:60-120): every two-stage */
+/* (light i < heavy j) and three-stage (light i < middle j < heavy k) point.  */
+/* ------------------------------------------------------------------------- */
+
+/* h[n]; scores[M][n] noise-free accept scores (frontier.py:52-57) and
+ * model_params[M][3] = {latency_s[1], base cost, hardness penalty}, both in
+ * latency order (M <= 16); thr_unique = sorted distinct thresholds (U).
+ * Outputs (lat, fid) float64 pairs:
+ *   out_two  [M(M-1)/2][U][U][2]         pairs   lexicographic, (theta, tau) ranks
+ *   out_three[M(M-1)(M-2)/6][U][U][U][2] triples lexicographic, (theta, tau1, tau2)
+ * Latencies are the reference's float expressions bit for bit; fidelities use
+ * fixed-point hardness sums (hadis_fid_exact gives numpy-exact two-stage values).
+ * bad_records counts hardness outside [0, 1]. */
+size_t hadis_cascade_workspace_bytes(int32_t n_models, int32_t n_unique);
+int hadis_cascade_points(const double* h, const double* scores, int64_t n, int32_t n_models,
+                         const double* model_params, const double* thr_unique, int32_t n_unique,
+                         int32_t hfix_shift, double* out_two, double* out_three,
+                         uint32_t* bad_records, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
 /* Generic pareto_prune (catalog.py:171-192) over n (latency, quality) keys:
  * out_idx receives the kept original indices in the reference's output order
  * ((latency, quality, index) ascending); out_count[0] their number.

@@ -50,6 +50,9 @@ _SIGNATURES = {
                                       _c_vp, _c_vp, _c_vp, _c_vp]),
     "hadis_fid_exact": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
                                  _c_vp]),
+    "hadis_cascade_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
+    "hadis_cascade_points": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_i32, _c_i32,
+                                      _c_vp, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_pareto_workspace_bytes": (_c_sz, [_c_i64]),
     "hadis_pareto_prune": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_solve_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),

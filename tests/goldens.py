@@ -49,3 +49,7 @@ def scores_of(rec):
 
 
 PROFILE_CASES = ("ties3000", "geo8", "cross1500")
+
+
+def frontier_cases():
+    return {d["name"]: d for d in load_json("frontier")}

@@ -330,3 +330,60 @@ def test_sharded_profile_equals_single(gpu_device, world):
                          capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "sharded OK" in out.stdout
+
+
+# ------------------------------------------------ cascade-depth frontier (f1)
+
+def _frontier_case(name):
+    from tests.goldens import frontier_cases
+    d = frontier_cases()[name]
+    return d, catalog_from_doc(d["catalog"]), np.asarray(d["h"]), tuple(d["thresholds"])
+
+
+def _hull_close(got, want, tol=1e-9):
+    """Envelopes agree as functions: values at every breakpoint of both."""
+    from paper_2509_00642_b200.frontier import envelope_value
+    want = [tuple(p) for p in want]
+    xs = sorted({x for x, _ in got} | {x for x, _ in want})
+    lo, hi = max(got[0][0], want[0][0]), min(got[-1][0], want[-1][0])
+    assert abs(got[0][0] - want[0][0]) <= tol and abs(got[-1][0] - want[-1][0]) <= tol
+    for x in xs:
+        if lo <= x <= hi:
+            assert abs(envelope_value(got, x) - envelope_value(want, x)) <= tol * max(1.0, abs(x))
+
+
+@pytest.mark.parametrize("name", ["jitter%02d" % s for s in range(20)] +
+                         ["wide", "default", "default_k33_n2000", "wide_dupgrid"])
+def test_frontier_compare_matches_reference(gpu_device, name):
+    from paper_2509_00642_b200.frontier import frontier_compare
+    d, cat, h, thr = _frontier_case(name)
+    rep = frontier_compare(cat, h=h, thresholds=thr)
+    r = d["report"]
+    assert (rep.n_two, rep.n_three) == (r["n_two"], r["n_three"])
+    assert abs(rep.gap - r["gap"]) <= 1e-9
+    _hull_close(list(rep.envelope_two), r["envelope_two"])
+    _hull_close(list(rep.envelope_three), r["envelope_three"])
+
+
+@pytest.mark.parametrize("name", ["jitter00", "wide", "wide_dupgrid"])
+def test_cascade_points_match_reference(gpu_device, name):
+    """Two-stage points bit-exact (latency and numpy-exact fidelity); three-stage
+    latency bit-exact, fidelity within 1e-12 relative."""
+    from paper_2509_00642_b200.frontier import three_stage_points, two_stage_points
+    d, cat, h, thr = _frontier_case(name)
+    two = two_stage_points(cat.variants, h, thr)
+    assert [[p.latency_s, p.fidelity_cost, list(p.detail)] for p in two] == d["two"]
+    three = three_stage_points(cat.variants, h, thr)
+    assert len(three) == len(d["three"])
+    for p, (lat, fid, det) in zip(three, d["three"]):
+        assert p.latency_s == lat and list(p.detail) == det
+        assert math.isclose(p.fidelity_cost, fid, rel_tol=1e-12)
+
+
+def test_frontier_errors(gpu_device):
+    from paper_2509_00642_b200.frontier import FrontierError, frontier_compare, lower_envelope
+    cat = default_catalog()
+    with pytest.raises(FrontierError):
+        frontier_compare(cat, h=np.array([0.5, 1.5]))
+    with pytest.raises(FrontierError):
+        lower_envelope([])
