@@ -114,23 +114,75 @@ class CascadePoints:
         _lib.check(lib.hadis_cascade_points(p(d_h), p(d_s), n, M, p(d_p), p(d_u), U, shift,
                                             p(out2), p(out3), p(bad), p(ws), ws_bytes, st),
                    "hadis_cascade_points")
+        self._d = (d_h, d_s, params, n, U, M)
         if exact and P2:
-            # numpy-exact two-stage fidelities: mean of where(h > theta | s_i < tau, c_j, c_i)
-            pairs = [(i, j) for i in range(M) for j in range(i + 1, M)]
-            cells = [(i, a, b, j) for (i, j) in pairs for a in range(U) for b in range(U)]
-            slot = torch.tensor([c[0] for c in cells], dtype=torch.int32, device=dev)
-            th = torch.tensor([self.unique[c[1]] for c in cells], dtype=torch.float64, device=dev)
-            ta = torch.tensor([self.unique[c[2]] for c in cells], dtype=torch.float64, device=dev)
-            cp = torch.tensor([(params[c[0], 1], params[c[0], 2], params[c[3], 1], params[c[3], 2])
-                               for c in cells], dtype=torch.float64, device=dev)
-            fid = torch.empty(len(cells), dtype=torch.float64, device=dev)
-            _lib.check(lib.hadis_fid_exact(p(d_h), p(d_s), n, len(cells), p(slot), p(th), p(ta),
-                                           p(cp), p(fid), st), "hadis_fid_exact")
-            out2[..., 1] = fid.view(P2, U, U)
+            out2.view(-1, 2)[:, 1] = self.exact_two(np.arange(P2 * U * U))
         if int(bad.item()):
             raise FrontierError("frontier: hardness must be finite and within [0, 1]")
-        self.two = out2.cpu().numpy()
-        self.three = out3.cpu().numpy()[:P3]
+        self._dev = (out2, out3[:P3])
+        self._two = self._three = None
+
+    def exact_two(self, flat):
+        """numpy-exact two-stage fidelities (hadis_fid_exact: the pairwise mean of
+        where(h > theta | s_i < tau, c_j, c_i)) for flat indices into ``two``."""
+        torch = _lib.torch_cuda()
+        d_h, d_s, params, n, U, M = self._d
+        flat = np.asarray(flat, dtype=np.int64)
+        pairs = np.array([(i, j) for i in range(M) for j in range(i + 1, M)], dtype=np.int64)
+        pr, a, b = flat // (U * U), flat // U % U, flat % U
+        li, hj = pairs[pr, 0], pairs[pr, 1]
+        u = np.asarray(self.unique)
+        dev = d_h.device
+        slot = torch.from_numpy(li.astype(np.int32)).to(dev)
+        th = torch.from_numpy(u[a]).to(dev)
+        ta = torch.from_numpy(u[b]).to(dev)
+        cp = torch.from_numpy(np.stack([params[li, 1], params[li, 2], params[hj, 1],
+                                        params[hj, 2]], axis=1)).to(dev)
+        fid = torch.empty(flat.size, dtype=torch.float64, device=dev)
+        if flat.size:
+            p = _lib.ptr
+            _lib.check(_lib.load().hadis_fid_exact(p(d_h), p(d_s), n, int(flat.size), p(slot),
+                                                   p(th), p(ta), p(cp), p(fid),
+                                                   _lib.stream_handle()), "hadis_fid_exact")
+        return fid
+
+    @property
+    def two(self):
+        if self._two is None:
+            self._two = self._dev[0].cpu().numpy()
+        return self._two
+
+    @property
+    def three(self):
+        if self._three is None:
+            self._three = self._dev[1].cpu().numpy()
+        return self._three
+
+    def hull_candidates(self, which, exact_two=False):
+        """(lat, fid) of the points that can be lower-envelope vertices: the
+        left and right Pareto staircases (hadis_pareto_prune on (lat, fid) and
+        (-lat, fid)); every other point is beaten in fidelity from both sides
+        and lies strictly above the envelope."""
+        torch = _lib.torch_cuda()
+        pts = self._dev[0 if which == 2 else 1].reshape(-1, 2)
+        lat, fid = pts[:, 0].contiguous(), pts[:, 1].contiguous()
+        lib = _lib.load()
+        n = int(lat.numel())
+        ws_bytes = lib.hadis_pareto_workspace_bytes(n)
+        ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=lat.device)
+        keep = []
+        for x in (lat, -lat):
+            idx = torch.empty(n, dtype=torch.int64, device=lat.device)
+            cnt = torch.zeros(1, dtype=torch.int64, device=lat.device)
+            _lib.check(lib.hadis_pareto_prune(_lib.ptr(x), _lib.ptr(fid), n, _lib.ptr(idx),
+                                              _lib.ptr(cnt), _lib.ptr(ws), ws_bytes,
+                                              _lib.stream_handle()), "hadis_pareto_prune")
+            keep.append(idx[:int(cnt.item())])
+        sel = torch.unique(torch.cat(keep))
+        f = fid[sel]
+        if which == 2 and exact_two:
+            f = self.exact_two(sel.cpu().numpy())
+        return lat[sel].cpu().numpy(), f.cpu().numpy()
 
     def two_points(self):
         vs, thr, r = self.variants, self.thresholds, self.rank
@@ -257,9 +309,10 @@ def frontier_compare(catalog, h: np.ndarray | None = None, thresholds=THRESHOLDS
         raise FrontierError("two_stage_points: need at least two variants")
     if len(variants) < 3:
         raise FrontierError("three_stage_points: need at least three variants")
-    cp = CascadePoints(variants, h, thresholds, exact=exact)
-    env2 = _hull_xy(cp.two[..., 0], cp.two[..., 1])
-    env3 = _hull_xy(cp.three[..., 0], cp.three[..., 1])
+    # exact two-stage fidelities only where they matter: the envelope candidates
+    cp = CascadePoints(variants, h, thresholds, exact=False)
+    env2 = _hull_xy(*cp.hull_candidates(2, exact_two=exact))
+    env3 = _hull_xy(*cp.hull_candidates(3))
     K = len(cp.thresholds)
     M = len(cp.variants)
     return FrontierReport(gap=envelope_gap(env2, env3), envelope_two=tuple(env2),
