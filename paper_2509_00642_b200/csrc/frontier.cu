@@ -874,6 +874,25 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
       const int64_t s0 = (int64_t)boff[key];
       const int64_t s1 = min(s0 + (int64_t)bcnt[key], m);
       if (s0 >= w0 && s1 <= w1) {
+        // fast certified pass: branch-free over the staged mates; only a
+        // near-tie (with G or with a mate at lower-or-equal latency) takes the
+        // full decide_one path
+        const double d2 = pcs[p].delta2;
+        const double G = __ddiv_rn(gpre[key], (double)g.n);
+        const double lo = cd.fid - d2, hi = cd.fid + d2;
+        bool kill = G < lo, close = G <= hi && !kill;
+        const double2* sm = s_lf - w0;
+        for (int64_t j = s0; j < s1; ++j) {
+          const double2 lf = sm[j];
+          const bool le = lf.x <= cd.lat;
+          kill |= le & (lf.y < lo);
+          close |= le & (lf.y <= hi) & (j != i);
+        }
+        if (kill) continue;
+        if (!close) {
+          set_bit(o.kept_bm, (int64_t)p * g.bm_stride + cd.cell);
+          continue;
+        }
         decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, gpre[key], grp, s0, s1, i, o,
                    [&](int64_t j) { return s_lf[j - w0]; });
       } else {
