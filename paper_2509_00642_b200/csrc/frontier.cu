@@ -381,17 +381,31 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
     for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = ~0ull;
     for (int w0 = 0; w0 < g.U; w0 += kRowWin) {
       __syncwarp();
-      for (int i = lane; i < kRowWin; i += 32) {       // stage (coalesced loads)
-        const int t = w0 + i;
+      // stage: all kRowT coalesced loads of the window in flight, then convert
+      uint32_t nrv[kRowT];
+      uint64_t shv[kRowT];
+#pragma unroll
+      for (int r = 0; r < kRowT; ++r) {
+        const int t = w0 + r * 32 + lane;
+        nrv[r] = t < g.U ? C[rk + t] : 0u;
+        shv[r] = t < g.U ? Sh[rk + t] : 0ull;
+      }
+      uint32_t prev = w0 > 0 ? C[rk + w0 - 1] : 0u;  // C at the cell before the window
+#pragma unroll
+      for (int r = 0; r < kRowT; ++r) {
+        const int i = r * 32 + lane, t = w0 + i;
         const int at = (i % kRowT) * kRowPad + i / kRowT;
+        uint32_t left = __shfl_up_sync(0xffffffffu, nrv[r], 1);
+        if (lane == 0) left = prev;
+        prev = __shfl_sync(0xffffffffu, nrv[r], 31);
         if (t < g.U) {
-          const uint32_t nr = C[rk + t];
-          const uint64_t SH = Hnb + Sh[rk + t];
+          const uint32_t nr = nrv[r];
+          const uint64_t SH = Hnb + shv[r];
           const uint32_t nH = (n - Rk) + nr;
           s_nH[at] = (double)nH;
           s_SHs[at] = __dmul_rn((double)SH, inv);
           s_LP[at] = light_part(bl, pl, (double)(n - nH), __dmul_rn((double)(Htot - SH), inv));
-          s_cls[at] = t == 0 || nr != C[rk + t - 1];
+          s_cls[at] = t == 0 || nr != left;
         } else {                                         // past the row end: S = +inf
           s_nH[at] = 0.0;
           s_SHs[at] = 0.0;
