@@ -37,8 +37,8 @@ constexpr int kGuide = 4096;          // guide buckets over [0, 1]
 constexpr int kMaxBins = 2048;        // U + 1 <= kMaxBins (u16 bins)
 constexpr int kRowChunk = 32768;      // records per K1 CTA: 2^15 * 2^16 < 2^31 per limb
 constexpr int kK1Threads = 512;
-constexpr int kBkThreads = 512;       // scatter CTA
-constexpr int kBkTile = 4096;         // records per scatter tile
+constexpr int kBkThreads = 1024;      // scatter CTA
+constexpr int kBkTile = 8192;         // records per scatter tile
 constexpr int kBkPer = kBkTile / kBkThreads;   // records per thread per tile (even)
 constexpr int kCountThreads = 512;
 
@@ -54,6 +54,7 @@ struct RowPlan {
   uint32_t* guide_le;    // [kGuide + 1]
   uint32_t* bad;         // [1]
   uint32_t* sparse;      // [1] nonzero: some guide bucket holds > 2 thresholds
+  uint32_t* nonuniform;  // [1] nonzero: thresholds are not exactly i / (U - 1)
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -77,12 +78,13 @@ __host__ __device__ inline RowPlan row_plan_at(void* base) {
   r.guide_le = (uint32_t*)(p + o);    o += align256(4 * (kGuide + 1));
   r.bad = (uint32_t*)(p + o);         o += align256(4);
   r.sparse = (uint32_t*)(p + o);      o += align256(4);
+  r.nonuniform = (uint32_t*)(p + o);  o += align256(4);
   return r;
 }
 
 static size_t row_plan_size() {
   return align256(4 * kMaxBins) * 2 + align256(8 * (kMaxBins + 1)) * 2 + align256(8 * kMaxBins) +
-         align256(kMaxBins) + align256(4 * (kGuide + 1)) * 2 + align256(4) * 2;
+         align256(kMaxBins) + align256(4 * (kGuide + 1)) * 2 + align256(4) * 3;
 }
 
 // #{u < x} (kLE = false) or #{u <= x} (kLE = true) over sorted unique u, with
@@ -102,6 +104,27 @@ __device__ __forceinline__ int guided_bin_dense(const double* u, int U, const ui
     return b + (kLE ? (u0 <= x) + (u1 <= x) : (u0 < x) + (u1 < x));
   }
   return kLE ? count_less_equal(u, U, x) : count_less(u, U, x);
+}
+
+// Uniform grid u[i] = i / (U - 1) (rp.nonuniform == 0): g = trunc(x (U - 1)) is
+// within one of the answer, so two independent compares finish it
+// (u[g - 1] <= x always holds; u padded with +inf).
+template <bool kLE>
+__device__ __forceinline__ int uniform_bin(const double* u, int U, double x) {
+  if (x >= 0.0 && x <= 1.0) {
+    const int g = min(__double2int_rz(x * (double)(U - 1)), U - 1);
+    const double u0 = u[g], u1 = u[g + 1];
+    return g + (kLE ? (u0 <= x) + (u1 <= x) : (u0 < x) + (u1 < x));
+  }
+  return kLE ? count_less_equal(u, U, x) : count_less(u, U, x);
+}
+
+// the cheapest exact binning the plan allows: 0 uniform, 1 dense guide, 2 general
+template <bool kLE>
+__device__ __forceinline__ int plan_bin(int mode, const double* u, int U, const uint32_t* guide,
+                                        double x) {
+  return mode == 0 ? uniform_bin<kLE>(u, U, x)
+                   : (mode == 1 ? guided_bin_dense<kLE>(u, U, guide, x) : guided_bin<kLE>(u, U, guide, x));
 }
 
 template <bool kLE>
@@ -127,6 +150,7 @@ __device__ __forceinline__ int guided_bin(const double* u, int U, const uint32_t
 __global__ void bucket_setup_kernel(const double* __restrict__ thr, int U, RowPlan rp) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < kMaxBins) rp.row_cnt[j] = 0;
+  if (j < U && (U < 2 || thr[j] != (double)j / (double)(U - 1))) atomicOr(rp.nonuniform, 1u);
   if (j > kGuide + 1) return;
   auto cnt = [&](double x, bool le) {
     int lo = 0, hi = U;
@@ -158,7 +182,7 @@ bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __res
   for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) s_guide[i] = rp.guide_lt[i];
   for (int i = threadIdx.x; i < U + 2; i += blockDim.x) s_thr[i] = i < U ? thr[i] : INFINITY;
   __syncthreads();
-  const bool dense = *rp.sparse == 0;
+  const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
   uint32_t my_bad = 0;
   const int64_t n2 = n >> 1;
   const double2* h2 = reinterpret_cast<const double2*>(h);
@@ -166,8 +190,7 @@ bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __res
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   auto one = [&](double x) {
     my_bad += !(x >= 0.0 && x <= 1.0);
-    atomicAdd(&s_cnt[dense ? guided_bin_dense<false>(s_thr, U, s_guide, x)
-                           : guided_bin<false>(s_thr, U, s_guide, x)], 1u);
+    atomicAdd(&s_cnt[plan_bin<false>(mode, s_thr, U, s_guide, x)], 1u);
   };
   if (vec) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
@@ -262,7 +285,7 @@ __device__ __forceinline__ void write_out(int cnt, F&& store) {
 // owns records tile0 + 2*(j*kBkThreads + i) + {0, 1}, j < kBkPer/2, so each
 // warp load is one 512-byte 128-bit-per-lane transaction.
 template <bool kVec>
-__global__ void __launch_bounds__(kBkThreads, 2)
+__global__ void __launch_bounds__(kBkThreads, 1)
 bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
                       int n_light, const double* __restrict__ thr, int U, double hscale,
                       RowPlan rp, uint64_t* __restrict__ hfix_rows, uint16_t* __restrict__ bs_rows) {
@@ -284,7 +307,7 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
   for (int i = threadIdx.x; i < U + 2; i += blockDim.x) s_thr[i] = i < U ? thr[i] : INFINITY;
   const int B1 = U + 1;
   const int64_t tiles = ceil_div(n, kBkTile);
-  const bool dense = *rp.sparse == 0;
+  const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
   constexpr int kP = kBkPer / 2;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kBkTile;
@@ -310,8 +333,7 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
       for (int e = 0; e < 2; ++e) {
         if (r + e < tn) {
           const double x = xs[e];
-          const int b = dense ? guided_bin_dense<false>(s_thr, U, s_guide_lt, x)
-                              : guided_bin<false>(s_thr, U, s_guide_lt, x);
+          const int b = plan_bin<false>(mode, s_thr, U, s_guide_lt, x);
           const uint32_t rank = atomicAdd(&s_cnt[b], 1u);
           key[2 * j + e] = ((uint32_t)b << 16) | rank;
           hf[2 * j + e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
@@ -380,7 +402,11 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
       const int qm = l % kQuad;
       if (qm == 0) __syncthreads();      // previous quad (or hfix) fully written out
       uint16_t* st = s_st16 + qm * kBkTile;
-      if (dense) {
+      if (mode == 0) {
+#pragma unroll
+        for (int e = 0; e < kBkPer; ++e)
+          if (key[e] != 0xffffffffu) st[key[e]] = (uint16_t)uniform_bin<true>(s_thr, U, sv[e]);
+      } else if (mode == 1) {
 #pragma unroll
         for (int e = 0; e < kBkPer; ++e)
           if (key[e] != 0xffffffffu)
@@ -593,7 +619,7 @@ extern "C" int hadis_records_plan(const double* h, int64_t n, const double* thr_
   cudaStream_t st = (cudaStream_t)stream;
   const RowPlan rp = row_plan_at(row_plan);
   const double hscale = ldexp(1.0, hfix_shift);
-  HADIS_CUDA_TRY(cudaMemsetAsync(rp.bad, 0, 256 * 2, st));      // bad + sparse flags
+  HADIS_CUDA_TRY(cudaMemsetAsync(rp.bad, 0, 256 * 3, st));      // bad, sparse, nonuniform
   bucket_setup_kernel<<<(unsigned)ceil_div(kGuide + 2, 256), 256, 0, st>>>(thr_unique, n_unique, rp);
   HADIS_LAUNCH_CHECK();
   const size_t csmem = (size_t)4 * (kMaxBins + kGuide + 2) + (size_t)8 * (n_unique + 2);
@@ -629,7 +655,7 @@ extern "C" int hadis_records_scatter(const double* h, const double* scores, int6
   auto kern = vec ? bucket_scatter_kernel<true> : bucket_scatter_kernel<false>;
   HADIS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
   int64_t sgrid = ceil_div(n, kBkTile);
-  if (sgrid > kNumSMs * 2) sgrid = kNumSMs * 2;
+  if (sgrid > kNumSMs) sgrid = kNumSMs;
   kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
                                                    hscale, rp, hfix_rows, bs_rows);
   HADIS_LAUNCH_CHECK();

@@ -272,7 +272,8 @@ def test_k1_layouts_agree(gpu_device, layout):
 
 
 @pytest.mark.parametrize("n,thr_k,shift_case", [(100_001, 48, "odd"), (262_144, 64, "wide"),
-                                                 (3, 5, "tiny"), (70_000, 1024, "k1024")])
+                                                 (3, 5, "tiny"), (70_000, 1024, "k1024"),
+                                                 (50_000, 200, "random"), (50_000, 64, "clustered")])
 def test_bucketed_histograms_bitexact(gpu_device, n, thr_k, shift_case):
     """The row-bucketed store + K1 give bit-identical prefix tables to the
     global-atomic K1 on adversarial records: hardness exactly on thresholds,
@@ -282,7 +283,11 @@ def test_bucketed_histograms_bitexact(gpu_device, n, thr_k, shift_case):
     rng = np.random.default_rng(n + thr_k)
     cat = default_catalog()
     pool = select_candidates(cat, 0.1, 0.1)
-    thr = tuple(i / (thr_k - 1) for i in range(thr_k))
+    thr = tuple(i / (thr_k - 1) for i in range(thr_k))      # uniform-grid binning path
+    if shift_case == "random":                               # guided (<= 2 per guide bucket)
+        thr = tuple(sorted(set(np.round(rng.uniform(0, 1, thr_k), 6).tolist())))
+    elif shift_case == "clustered":                          # general guided search
+        thr = tuple(sorted(set((0.5 + rng.uniform(-1e-4, 1e-4, thr_k)).tolist() + [0.0, 1.0])))
     h = rng.uniform(0.0, 1.0, n)
     pick = rng.random(n)
     h[pick < 0.2] = rng.choice(np.asarray(thr), int((pick < 0.2).sum()))
