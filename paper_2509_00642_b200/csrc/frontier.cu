@@ -326,6 +326,7 @@ struct Cands {
 // repeat an earlier row's R[k] (same row class) are exact duplicates and are
 // skipped.
 constexpr int kRowWarps = 8;
+constexpr int kCoarseShift = 4;      // F1/F3 latency buckets: the fine ones >> 4
 constexpr int kMaxGroup = 64;        // heavy partners per light slot (pool <= 65 models)
 constexpr int kRowT = 8;             // cells per lane per window
 constexpr int kRowWin = 32 * kRowT;  // cells per window
@@ -475,13 +476,19 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
   const double* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
                                             const unsigned long long* key, unsigned take) {
-    unsigned long long* const bp = bmin + (int64_t)p * g.nbuckets;
+    unsigned long long* const bp = bmin + (int64_t)p * (g.nbuckets >> kCoarseShift);
     const double xr = __dmul_rn(dRk, pc.Ll);
     int bk[kRowT];
     unsigned long long cur[kRowT];
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)
-      bk[j] = bucket_of_x(pc, g.nbuckets, __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)));
+      bk[j] = bucket_of_x(pc, g.nbuckets,
+                          __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh))) >> kCoarseShift;
+    // row-frontier keys strictly decrease along the walk: of consecutive taken
+    // cells in one coarse bucket only the last can lower its minimum
+#pragma unroll
+    for (int j = 0; j + 1 < kRowT; ++j)
+      if ((take >> (j + 1) & 1u) && bk[j + 1] == bk[j]) take &= ~(1u << j);
 #pragma unroll
     for (int j = 0; j < kRowT; ++j) cur[j] = (take >> j & 1u) ? bp[bk[j]] : 0ull;
 #pragma unroll
@@ -785,7 +792,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const double* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
                                            const unsigned long long* key, unsigned take) {
-    const double* const gp = gpre + (int64_t)p * g.nbuckets;
+    const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
     const double xr = __dmul_rn(dRk, pc.Ll);
     int bk[kRowT];
     double gv[kRowT];
@@ -793,7 +800,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
     for (int j = 0; j < kRowT; ++j)
       bk[j] = bucket_of_x(pc, g.nbuckets, __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)));
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j]] : -INFINITY;
+    for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j] >> kCoarseShift] : -INFINITY;
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)
       if (!(from_order_key(key[j]) <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
@@ -830,15 +837,20 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
 __global__ void group_cands_kernel(Cands lst, const unsigned long long* __restrict__ n_list,
                                    int64_t cap, int nbuckets, double dn,
                                    const unsigned long long* __restrict__ boff,
-                                   uint32_t* __restrict__ bcur, Cands grp) {
+                                   uint32_t* __restrict__ bcur, Cands grp,
+                                   unsigned long long* __restrict__ fmin) {
   if ((int64_t)*n_list > cap) return;
   const int64_t m = (int64_t)*n_list;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     Cand cd = lst.c[i];
+    const int64_t key = (int64_t)cd.pair * nbuckets + cd.bucket;
+    // fine-bucket minima over the candidates: every cell F1/F3 pruned is
+    // beaten by a candidate at lower-or-equal latency, so the exclusive
+    // prefix of these minima is the exact fine G
+    atomicMin(&fmin[key], (unsigned long long)order_key(cd.fid));
     cd.lat = __ddiv_rn(cd.lat, dn);       // the list holds raw numerators
     cd.fid = __ddiv_rn(cd.fid, dn);
-    const int64_t key = (int64_t)cd.pair * nbuckets + cd.bucket;
     grp.c[(int64_t)boff[key] + atomicAdd(&bcur[key], 1u)] = cd;
   }
 }
@@ -1349,7 +1361,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
+  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
       counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
 };
 
@@ -1371,6 +1383,9 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.tsum = take(8 * (ceil_div(pb, 4096) + 1));
   L.bmin = take(8 * pb);
   L.gpre = take(8 * pb);
+  L.cmin = take(8 * (pb >> kCoarseShift));
+  L.cpre = take(8 * (pb >> kCoarseShift));
+  L.ctmin = take(8 * (ceil_div(nbuckets >> kCoarseShift, 4096) * n_pairs + 1));
   L.bcnt = take(4 * pb);
   L.bcur = take(4 * pb);
   L.boff = take(8 * (pb + 1));
@@ -1449,6 +1464,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   unsigned long long* tsum = (unsigned long long*)P(L.tsum);
   unsigned long long* bmin = (unsigned long long*)P(L.bmin);
   double* gpre = (double*)P(L.gpre);
+  unsigned long long* cmin = (unsigned long long*)P(L.cmin);
+  double* cpre = (double*)P(L.cpre);
+  unsigned long long* ctmin = (unsigned long long*)P(L.ctmin);
   uint32_t* bcnt = (uint32_t*)P(L.bcnt);
   uint32_t* bcur = (uint32_t*)P(L.bcur);
   unsigned long long* boff = (unsigned long long*)P(L.boff);
@@ -1476,6 +1494,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   const int64_t cells = (int64_t)n_unique * n_unique;
   const int64_t words_per_pair = (cells + 31) / 32;
   HADIS_CUDA_TRY(cudaMemsetAsync(bmin, 0xff, 8 * pb, st));
+  HADIS_CUDA_TRY(cudaMemsetAsync(cmin, 0xff, 8 * (pb >> kCoarseShift), st));
   HADIS_CUDA_TRY(cudaMemsetAsync(bcnt, 0, 4 * pb, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(bcur, 0, 4 * pb, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(kept, 0, 4 * words_per_pair * n_pairs, st));
@@ -1484,7 +1503,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
-  int launches = 28;   // fixed kernels below; batched emulation adds 2 per batch
+  int launches = 31;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
@@ -1499,15 +1518,16 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
   HADIS_CUDA_TRY(cudaFuncSetAttribute(filter_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-  bucket_min_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, bmin);
-  {
-    const int tiles = (int)ceil_div(nb, kPrefTile);
-    prefix_tile_min_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin);
-    prefix_carry_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(tmin, tiles, n_pairs);
-    prefix_apply_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(bmin, nb, tmin, gpre);
-  }
+  bucket_min_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cmin);
+  auto prefix = [&](const unsigned long long* mins, int nbk, unsigned long long* tm, double* pre) {
+    const int tiles = (int)ceil_div(nbk, kPrefTile);
+    prefix_tile_min_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(mins, nbk, tm);
+    prefix_carry_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(tm, tiles, n_pairs);
+    prefix_apply_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(mins, nbk, tm, pre);
+  };
+  prefix(cmin, nb >> kCoarseShift, ctmin, cpre);
   const DecideOut dout{kept, un, exact_cap, reqbm, req_pair, req_cell, exact_cap, counters};
-  filter_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, gpre, bcnt, lst,
+  filter_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cpre, bcnt, lst,
                                                      cand_cap, counters + 5);
   {
     const int64_t tiles = ceil_div(pb, kScanTile);
@@ -1517,8 +1537,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
   group_cands_kernel<<<kNumSMs * 8, 256, 0, st>>>(lst, counters + 5, cand_cap, nb, (double)n, boff,
-                                                  bcur,
-                                                  grp);
+                                                  bcur, grp, bmin);
+  prefix(bmin, nb, tmin, gpre);                    // exact fine G for decide
   HADIS_LAUNCH_CHECK();
   decide_kernel<<<kNumSMs * 8, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
