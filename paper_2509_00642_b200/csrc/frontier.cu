@@ -184,8 +184,16 @@ __device__ __forceinline__ bool class_start(const Grid& g, const uint32_t* C, in
 }
 
 // Rank with the smallest first position in the tau-run of row k containing t.
-__device__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t, bool run_start = false) {
+__device__ __noinline__ int rep_tau_search(const Grid& g, const uint32_t* C, int k, int t);
+
+__device__ __forceinline__ int rep_tau(const Grid& g, const uint32_t* C, int k, int t,
+                                       bool run_start = false) {
   if (run_start && *g.sorted) return t;       // smallest rank == smallest position
+  return rep_tau_search(g, C, k, t);
+}
+
+// first_pos-smallest rank of t's duplicate run (binary searches along the row)
+__device__ __noinline__ int rep_tau_search(const Grid& g, const uint32_t* C, int k, int t) {
   const uint32_t* row = C + (int64_t)k * g.B1;
   const uint32_t v = row[t];
   int lo = 0, hi = t;                         // first index with row[idx] == v
@@ -788,6 +796,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
   const int lane = threadIdx.x & 31;
   const uint32_t krep = (uint32_t)g.row_rep[k] * (uint32_t)g.U;
+  const bool sorted_thr = *g.sorted != 0;          // first_pos increasing: rep = own rank
   const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
   const double* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
@@ -824,7 +833,8 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
       if (at < cap) {
         // raw numerators; F5 divides (lat = x / n, fid* = S / n)
         const int t = w0 + lane * kRowT + j;
-        lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)rep_tau(g, C, k, t, true), (uint32_t)bk[j], 0u,
+        lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
+                         (uint32_t)bk[j], 0u,
                          __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)),
                          from_order_key(key[j])};
       }
