@@ -580,6 +580,28 @@ row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs
   }
 }
 
+// Before K1 (row_scanned path): one warp per (light model, row).  Empty rows
+// are written as zeros -- already their own prefix -- and flagged scanned;
+// rows split across K1 CTAs (atomics) are zeroed and left for K2's row pass;
+// every other row is written whole by one K1 CTA.
+__global__ void prep_rows_kernel(RowPlan rp, int n_light, int U, uint32_t* __restrict__ g_cnt,
+                                 unsigned long long* __restrict__ g_hsum,
+                                 uint8_t* __restrict__ row_scanned) {
+  const int B1 = U + 1;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= (int64_t)n_light * B1) return;
+  const int k = (int)(row % B1);
+  const uint32_t c = rp.row_cnt[k];
+  const bool zero = c == 0 || c > (uint32_t)kRowChunk;
+  if (zero) {
+    uint32_t* gc = g_cnt + row * B1;
+    unsigned long long* gh = g_hsum + row * B1;
+    for (int i = lane; i < B1; i += 32) { gc[i] = 0u; gh[i] = 0ull; }
+  }
+  if (lane == 0) row_scanned[row] = c == 0;
+}
+
 static size_t scatter_smem(int U) {
   return (size_t)8 * kBkTile + (size_t)4 * (kBkTile + 2 * kMaxBins + 2 * (kGuide + 2)) +
          (size_t)8 * (U + 2);
@@ -689,9 +711,16 @@ extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs
   const int64_t bins = B1 * B1 * n_light;
   const int64_t max_items = ceil_div(n, kRowChunk) + n_unique + 1;
   if (max_items > 65535) return HADIS_ERR_UNSUPPORTED;
-  HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
-  HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
-  if (row_scanned) HADIS_CUDA_TRY(cudaMemsetAsync(row_scanned, 0, (size_t)B1 * n_light, st));
+  if (row_scanned) {
+    const int64_t rows = B1 * n_light;
+    prep_rows_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(
+        rp, n_light, n_unique, hist_cnt, (unsigned long long*)hist_hsum, row_scanned);
+    HADIS_LAUNCH_CHECK();
+    hadis_count_launches(1);
+  } else {
+    HADIS_CUDA_TRY(cudaMemsetAsync(hist_cnt, 0, bins * sizeof(uint32_t), st));
+    HADIS_CUDA_TRY(cudaMemsetAsync(hist_hsum, 0, bins * sizeof(uint64_t), st));
+  }
   const int B1s = (n_unique + 1) | 1;
   const size_t ksmem = (size_t)kQuad * 4 * B1s * 4;
   if (ksmem > 48 * 1024)
