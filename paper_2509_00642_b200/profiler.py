@@ -358,6 +358,32 @@ class GridProfiler:
         rec(5)
         return state
 
+    def graph(self, plan: ProfilePlan, exact_fid=False):
+        """Capture the whole device pipeline of ``plan`` (B0..F14, ~40 kernels
+        and memsets) into one CUDA graph.  An eager run first learns the
+        output capacities; ``replay()`` relaunches the graph and returns the
+        DeviceTable (a capacity overflow falls back to an eager rerun inside
+        ``finish`` and the graph is re-captured on the next call)."""
+        torch = self.torch
+        self.finish(self.launch(plan, exact_fid))          # learn capacities, allocate
+        torch.cuda.synchronize(self.device)
+        box = {}
+
+        def capture():
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                state = self.launch(plan, exact_fid)
+            box.update(graph=g, state=state, caps=plan.caps)
+
+        def replay():
+            if box.get("caps") != plan.caps:
+                capture()
+            box["graph"].replay()
+            return self.finish(box["state"])
+
+        capture()
+        return replay
+
     def _frontier(self, state, caps):
         torch = self.torch
         plan = state["plan"]
