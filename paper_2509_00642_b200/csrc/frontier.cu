@@ -884,58 +884,37 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
               const unsigned long long* __restrict__ counters_ro, int64_t cap,
               const unsigned long long* __restrict__ boff, const uint32_t* __restrict__ bcnt,
               const double* __restrict__ gpre, Cands grp, DecideOut o) {
-  __shared__ double2 s_lf[kDecWin];
   if ((int64_t)counters_ro[0] > cap) return;
   const int64_t m = (int64_t)counters_ro[0];
-  for (int64_t c0 = (int64_t)blockIdx.x * kDecChunk; c0 < m; c0 += (int64_t)gridDim.x * kDecChunk) {
-    const int64_t c1 = min(m, c0 + kDecChunk);
-    auto seg_of = [&](int64_t i, int64_t* a, int64_t* b) {
-      const int64_t key = (int64_t)grp.c[i].pair * g.nbuckets + grp.c[i].bucket;
-      *a = (int64_t)boff[key];
-      *b = min(*a + (int64_t)bcnt[key], m);
-    };
-    int64_t sa, sb, ea, eb;
-    seg_of(c0, &sa, &sb);
-    seg_of(c1 - 1, &ea, &eb);
-    const int64_t w0 = max(sa, c0 - (kDecWin - kDecChunk) / 2);
-    const int64_t w1 = min(eb, w0 + kDecWin);
-    __syncthreads();                               // previous chunk done with s_lf
-    for (int64_t j = w0 + threadIdx.x; j < w1; j += blockDim.x)
-      s_lf[j - w0] = make_double2(grp.c[j].lat, grp.c[j].fid);
-    __syncthreads();
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-      const Cand cd = grp.c[i];
-      const int p = (int)cd.pair;
-      const int64_t key = (int64_t)p * g.nbuckets + cd.bucket;
-      const int64_t s0 = (int64_t)boff[key];
-      const int64_t s1 = min(s0 + (int64_t)bcnt[key], m);
-      if (s0 >= w0 && s1 <= w1) {
-        // fast certified pass: branch-free over the staged mates; only a
-        // near-tie (with G or with a mate at lower-or-equal latency) takes the
-        // full decide_one path
-        const double d2 = pcs[p].delta2;
-        const double G = __ddiv_rn(gpre[key], (double)g.n);
-        const double lo = cd.fid - d2, hi = cd.fid + d2;
-        bool kill = G < lo, close = G <= hi && !kill;
-        const double2* sm = s_lf - w0;
-        for (int64_t j = s0; j < s1; ++j) {
-          const double2 lf = sm[j];
-          const bool le = lf.x <= cd.lat;
-          kill |= le & (lf.y < lo);
-          close |= le & (lf.y <= hi) & (j != i);
-        }
-        if (kill) continue;
-        if (!close) {
-          set_bit(o.kept_bm, (int64_t)p * g.bm_stride + cd.cell);
-          continue;
-        }
-        decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, gpre[key], grp, s0, s1, i, o,
-                   [&](int64_t j) { return s_lf[j - w0]; });
-      } else {
-        decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, gpre[key], grp, s0, s1, i, o,
-                   [&](int64_t j) { return make_double2(grp.c[j].lat, grp.c[j].fid); });
-      }
+  const double dn = (double)g.n;
+  // one thread per candidate; its bucket-mates are the neighbouring candidates
+  // of the same segment (L1-resident for the warp): a branch-free certified
+  // pass, the full decide_one logic only on near-ties
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Cand cd = grp.c[i];
+    const int p = (int)cd.pair;
+    const int64_t key = (int64_t)p * g.nbuckets + cd.bucket;
+    const int64_t s0 = (int64_t)boff[key];
+    const int64_t s1 = min(s0 + (int64_t)bcnt[key], m);
+    const double GS = gpre[key];
+    const double d2 = pcs[p].delta2;
+    const double G = __ddiv_rn(GS, dn);
+    const double lo = cd.fid - d2, hi = cd.fid + d2;
+    bool kill = G < lo, close = G <= hi && !kill;
+    for (int64_t j = s0; j < s1; ++j) {
+      const double lat_j = grp.c[j].lat, fid_j = grp.c[j].fid;
+      const bool le = lat_j <= cd.lat;
+      kill |= le & (fid_j < lo);
+      close |= le & (fid_j <= hi) & (j != i);
     }
+    if (kill) continue;
+    if (!close) {
+      set_bit(o.kept_bm, (int64_t)p * g.bm_stride + cd.cell);
+      continue;
+    }
+    decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, GS, grp, s0, s1, i, o,
+               [&](int64_t q) { return make_double2(grp.c[q].lat, grp.c[q].fid); });
   }
 }
 
