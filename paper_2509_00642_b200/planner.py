@@ -3,7 +3,9 @@
 Public surface mirrors pkg/src/cascadesim/planner.py:
 ``Plan`` (:40-78), ``PlannerError`` (:36), ``queue_delay`` (:81),
 ``update_estimate`` (:88), ``solve`` (:217-227), ``fallback_plan``
-(:170-214) and ``make_planner(mode="online")`` (:443-455), plus the batched
+(:170-214), the consumers ``PlanCache`` / ``cached_solve`` (:328-367), the
+baselines ``clipper_plan`` / ``proteus_plan`` / ``diffserve_plan``
+(:387-500) and every ``make_planner`` mode (:443-479), plus the batched
 ``solve_many`` used by re-plan sweeps.  Every (demand, SLO) point is decided
 on the device by ``hadis_solve_many`` with the reference's exact float64
 expressions and tie-breaks; this module only moves rows/points to the device
@@ -12,7 +14,7 @@ and turns the per-point result back into ``Plan`` objects.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -286,13 +288,143 @@ def fallback_plan(indexed_rows, catalog, lam, queues, workers, t_slo, alpha, lab
     return plan
 
 
+@dataclass
+class PlanCache:
+    """Reuse plans for nearby states instead of re-solving each epoch
+    (planner.py:328-351): mode 'd' keys on the binned demand estimate, 'dq'
+    also on the binned total backlog."""
+
+    mode: str
+    demand_bin_qps: float = 10.0
+    queue_bin: int = 12
+    entries: dict = field(default_factory=dict)
+    hits: int = 0
+    misses: int = 0
+
+    def __post_init__(self) -> None:
+        if self.mode not in ("d", "dq"):
+            raise PlannerError(f"cache mode must be 'd' or 'dq', got {self.mode!r}")
+
+    def key(self, lam: float, queues) -> tuple:
+        demand_key = int(lam // self.demand_bin_qps)
+        if self.mode == "d":
+            return (demand_key,)
+        return (demand_key, int(sum((queues or {}).values()) // self.queue_bin))
+
+
+def cached_solve(cache: PlanCache, table, catalog, lam: float, queues=None,
+                 workers: int = DEFAULT_WORKERS, t_slo: float = DEFAULT_T_SLO_S,
+                 alpha: float = DEFAULT_QUEUE_ALPHA):
+    """Solve through the cache (planner.py:354-367); returns (plan, was_cache_hit)."""
+    key = cache.key(lam, queues)
+    hit = cache.entries.get(key)
+    if hit is not None:
+        cache.hits += 1
+        return hit, True
+    plan = solve(table, catalog, lam, queues, workers, t_slo, alpha)
+    cache.entries[key] = plan
+    cache.misses += 1
+    return plan, False
+
+
+def expected_cost_uniform(variant) -> float:
+    """Mean quality cost over hardness uniform on [0, 1] (quality.py:68-70)."""
+    return variant.base_quality_cost + 0.5 * variant.hardness_penalty
+
+
+def _single_model_row(variant, theta: float = 1.0):
+    """Synthetic no-cascade row: one model serves everything (planner.py:373-384)."""
+    from .profiler import CascadeRow
+    return CascadeRow(light_id=variant.id, heavy_id=variant.id, theta=theta, tau=0.0,
+                      r_light=1.0, r_heavy=0.0, fidelity_cost=expected_cost_uniform(variant),
+                      mean_latency_s=variant.latency_s[1])
+
+
+_SLACK = 1e-9
+
+
+def clipper_plan(catalog, which: str, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
+                 t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA) -> Plan:
+    """Static single-model cluster (planner.py:387-421): all workers on the
+    fastest ('light') or slowest ('heavy') variant at the largest batch whose
+    path latency fits the deadline; flagged infeasible when demand exceeds
+    that capacity.  A handful of scalar comparisons: host arithmetic."""
+    if which not in ("light", "heavy"):
+        raise PlannerError(f"clipper_plan: which must be light/heavy, got {which!r}")
+    ordered = catalog.sorted_by_latency()
+    variant = ordered[0] if which == "light" else ordered[-1]
+    row = _single_model_row(variant)
+    queues = queues or {}
+    wait = queue_delay(queues.get(variant.id, 0.0), lam, alpha)
+    fits = [b for b in catalog.batch_sizes if variant.latency_s[b] + wait <= t_slo + _SLACK]
+    chosen = fits[-1] if fits else catalog.batch_sizes[0]
+    infeasible = not fits or lam > workers * variant.throughput_qps[chosen] + _SLACK
+    return Plan(row=row, workers={variant.id: workers}, batches={variant.id: chosen}, lam=lam,
+                queues=dict(queues), fidelity_cost=row.fidelity_cost,
+                path_latency_s=variant.latency_s[chosen] + wait, infeasible=infeasible,
+                label=f"clipper-{which}")
+
+
+def proteus_plan(catalog, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
+                 t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA,
+                 eps_latency: float = 0.1, eps_quality: float = 0.1) -> Plan:
+    """Accuracy-scaling baseline (planner.py:424-440): the same device search
+    over one single-model row per candidate variant."""
+    from .catalog import select_candidates
+    rows = [_single_model_row(v) for v in select_candidates(catalog, eps_latency, eps_quality)]
+    if lam < 0:
+        raise PlannerError("solve: negative demand")
+    return solve_many(rows, catalog, [lam], queues, workers, t_slo, alpha, "proteus")[0]
+
+
+def diffserve_plan(table, catalog, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
+                   t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA,
+                   light_id: str = "sd35-turbo", heavy_id: str = "sd35-large") -> Plan:
+    """Fixed-pair discriminator cascade, no bypass (planner.py:482-500): the
+    device search over the table's no-bypass rows of one pair."""
+    max_theta = max(r.theta for r in table.rows)
+    rows = [r for r in table.rows if r.light_id == light_id and r.heavy_id == heavy_id
+            and r.theta == max_theta]
+    if not rows:
+        raise PlannerError(f"diffserve_plan: table has no rows for pair {light_id}/{heavy_id}")
+    if lam < 0:
+        raise PlannerError("solve: negative demand")
+    return solve_many(rows, catalog, [lam], queues, workers, t_slo, alpha, "diffserve")[0]
+
+
+PLANNER_MODES = ("online", "cache-d", "cache-dq", "clipper-light", "clipper-heavy", "proteus",
+                 "diffserve")
+
+
 def make_planner(mode: str, table, catalog, workers: int = DEFAULT_WORKERS,
                  t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA, **kwargs):
-    """(lam, queues) -> (Plan, info) callable; the GPU implements mode 'online'."""
-    if mode != "online":
-        raise PlannerError(f"mode {mode!r} is not on the accelerated path; use cascadesim's "
-                           "make_planner for the baseline planners")
+    """(lam, queues) -> (Plan, info) callable for the simulator (planner.py:443-479):
+    'online' re-solves each epoch on the device, 'cache-d'/'cache-dq' reuse
+    plans keyed on binned demand (and backlog), the rest are the baselines."""
+    if mode == "online":
+        def fn(lam, queues):
+            return solve(table, catalog, lam, queues, workers, t_slo, alpha), {}
+        return fn
+    if mode in ("cache-d", "cache-dq"):
+        cache = PlanCache(mode=mode.split("-")[1], **kwargs)
 
-    def fn(lam, queues):
-        return solve(table, catalog, lam, queues, workers, t_slo, alpha), {}
-    return fn
+        def fn(lam, queues):
+            plan, hit = cached_solve(cache, table, catalog, lam, queues, workers, t_slo, alpha)
+            return plan, {"cache_hit": hit}
+        return fn
+    if mode in ("clipper-light", "clipper-heavy"):
+        which = mode.split("-")[1]
+
+        def fn(lam, queues):
+            return clipper_plan(catalog, which, lam, queues, workers, t_slo, alpha), {}
+        return fn
+    if mode == "proteus":
+        def fn(lam, queues):
+            return proteus_plan(catalog, lam, queues, workers, t_slo, alpha), {}
+        return fn
+    if mode == "diffserve":
+        def fn(lam, queues):
+            return diffserve_plan(table, catalog, lam, queues, workers, t_slo, alpha,
+                                  **kwargs), {}
+        return fn
+    raise PlannerError(f"unknown planner mode {mode!r}; pick from {PLANNER_MODES}")

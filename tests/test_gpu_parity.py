@@ -421,3 +421,39 @@ def test_graph_replay_matches_eager(gpu_device):
     got = replay()
     assert got.n_rows == fresh.n_rows
     assert torch.equal(got.fid, fresh.fid) and torch.equal(got.lat, fresh.lat)
+
+
+# --------------------------------- online consumers of the allocation search (f4)
+
+def test_planner_modes_match_reference(gpu_device):
+    """Every make_planner mode (online, cache-d/dq, clipper, proteus, diffserve)
+    over a 120-epoch (demand, backlog) sequence equals the reference's plans
+    field by field (tests/golden/make_golden_planner_modes.py)."""
+    from paper_2509_00642_b200.planner import PlannerError, make_planner
+    from paper_2509_00642_b200.profiler import CascadeRow
+    doc = load_json("planner_conftest")
+    modes = load_json("planner_modes")
+    cat = default_catalog()
+    rows = tuple(CascadeRow(**r) for r in doc["table"]["rows"])
+
+    class T:                                       # table stand-in: .rows is all planners use
+        pass
+    table = T()
+    table.rows = rows
+    for key, want_list in modes["runs"].items():
+        mode, workers, t_slo = key.split("|")
+        fn = make_planner(mode, table, cat, workers=int(workers), t_slo=float(t_slo), alpha=1.5)
+        for ep, want in zip(modes["epochs"], want_list):
+            if "error" in want:
+                with pytest.raises(PlannerError):
+                    fn(ep["lam"], dict(ep["queues"]))
+                continue
+            plan, info = fn(ep["lam"], dict(ep["queues"]))
+            w = want["plan"]
+            got_row = {k: getattr(plan.row, k) for k in w["row"]}
+            assert got_row == w["row"], (key, ep)
+            assert (plan.workers, plan.batches, plan.infeasible, plan.label) == \
+                (w["workers"], w["batches"], w["infeasible"], w["label"]), (key, ep)
+            assert plan.path_latency_s == w["path_latency_s"], (key, ep)
+            assert plan.fidelity_cost == w["fidelity_cost"] and plan.lam == w["lam"]
+            assert plan.queues == w["queues"] and info == want["info"], (key, ep)
