@@ -353,6 +353,7 @@ def run_ours(args, cfg):
         if not args.no_allocation:
             line["allocation_search"] = measure_allocation(torch, dev, args.steps)
             line["cascade_depth"] = measure_cascade(torch, dev, args.steps)
+            line["router_sweep"] = measure_router(torch, dev, args.steps)
         traffic = _ncu_traffic(cfg.name)
         if traffic:
             line["roofline"]["traffic"] = traffic
@@ -494,6 +495,33 @@ def measure_cascade(torch, dev, steps, n=1_000_000, k=64, models=8, cpu_points=3
             "envelope_vertices": [len(rep.envelope_two), len(rep.envelope_three)],
             "cpu_s_per_point": cpu_per_point, "cpu_points_per_s": 1.0 / cpu_per_point,
             "cpu_kind": "port", "cpu_points_sampled": cpu_points}
+
+
+def measure_router(torch, dev, steps, cpu_vectors=12):
+    """tune_weights' exhaustive sweep (3^8 - 1 weight vectors) on a
+    3000-prompt labeled corpus (feature matrix from the golden fixture, made by
+    the reference's router.features), GPU vs the reference numpy loop (oracle
+    port, sampled vectors)."""
+    from oracle import router as orr
+    from paper_2509_00642_b200.router import tune_weights_features
+    with np.load(os.path.join(ROOT, "tests", "golden", "router.npz")) as z:
+        mat, lab = z["noisy3000:features"], z["noisy3000:labels"]
+    tune_weights_features(mat, lab)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        w, thr, acc = tune_weights_features(mat, lab)
+    sweep_s = (time.perf_counter() - t0) / steps
+    grid = orr.weight_grid(mat.shape[1])
+    t0 = time.perf_counter()
+    for w_ in grid[::len(grid) // cpu_vectors][:cpu_vectors]:
+        orr.best_split(mat, lab, w_)
+    cpu_per_vec = (time.perf_counter() - t0) / cpu_vectors
+    return {"workload": f"f3: tune_weights over {len(grid)} weight vectors x {len(lab)} prompts",
+            "vectors": len(grid), "sweep_s": sweep_s, "vectors_per_s": len(grid) / sweep_s,
+            "acc": acc, "cpu_s_per_vector": cpu_per_vec,
+            "cpu_sweep_s_extrapolated": cpu_per_vec * len(grid), "cpu_kind": "port",
+            "cpu_vectors_sampled": cpu_vectors}
 
 
 def _ncu_traffic(name):

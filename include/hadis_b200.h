@@ -200,6 +200,21 @@ int hadis_cascade_points(const double* h, const double* scores, int64_t n, int32
                          uint32_t* bad_records, void* workspace, size_t workspace_bytes,
                          void* stream);
 
+/* ------------------------------------------------------------------------- */
+/* Router weight sweep (router.py:199-234)                      */
+/* ------------------------------------------------------------------------- */
+
+/* features[n][n_features] (row-major), labels[n] (1 = should bypass to the
+ * heavy model), weights[n_vectors][n_features] (normalized grid vectors).
+ * Per vector v: scores = features . w (numpy's float64 order on the reference
+ * machine), candidate thresholds = midpoints between consecutive distinct
+ * scores plus min - 1 and max + 1, predicted hard = score > threshold;
+ * out_acc[v] = best balanced accuracy (tp/n_pos + tn/n_neg)/2, out_threshold[v]
+ * = its first maximising threshold.  n <= 8192 (HADIS_ERR_UNSUPPORTED above). */
+int hadis_tune_weights(const double* features, const uint8_t* labels, int32_t n,
+                       int32_t n_features, const double* weights, int32_t n_vectors,
+                       int32_t n_pos, double* out_acc, double* out_threshold, void* stream);
+
 /* Generic pareto_prune (catalog.py:171-192) over n (latency, quality) keys:
  * out_idx receives the kept original indices in the reference's output order
  * ((latency, quality, index) ascending); out_count[0] their number.

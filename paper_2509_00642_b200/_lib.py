@@ -53,6 +53,8 @@ _SIGNATURES = {
     "hadis_cascade_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
     "hadis_cascade_points": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_i32, _c_i32,
                                       _c_vp, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "hadis_tune_weights": (_c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
+                                    _c_vp, _c_vp]),
     "hadis_pareto_workspace_bytes": (_c_sz, [_c_i64]),
     "hadis_pareto_prune": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_solve_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),

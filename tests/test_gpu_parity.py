@@ -457,3 +457,42 @@ def test_planner_modes_match_reference(gpu_device):
             assert plan.path_latency_s == w["path_latency_s"], (key, ep)
             assert plan.fidelity_cost == w["fidelity_cost"] and plan.lam == w["lam"]
             assert plan.queues == w["queues"] and info == want["info"], (key, ep)
+
+
+# ------------------------------------------------ router weight sweep (f3)
+
+@pytest.mark.parametrize("name", ["separable80", "noisy600", "noisy3000"])
+def test_tune_weights_matches_reference(gpu_device, name):
+    from paper_2509_00642_b200.router import tune_weights_features
+    d = {x["name"]: x for x in load_json("router")}[name]
+    arr = load_npz("router")
+    w, thr, acc = tune_weights_features(arr[name + ":features"], arr[name + ":labels"])
+    assert (list(w), thr, acc) == (d["weights"], d["threshold"], d["acc"])
+
+
+def test_tune_weights_per_vector_matches_reference(gpu_device):
+    import torch
+    from paper_2509_00642_b200 import _lib
+    from paper_2509_00642_b200.router import _weight_grid
+    d = {x["name"]: x for x in load_json("router")}["separable80"]
+    arr = load_npz("router")
+    mat, lab = arr["separable80:features"], arr["separable80:labels"]
+    grid = _weight_grid(mat.shape[1], (0.0, 1.0, 2.0))
+    dev = torch.device("cuda")
+    acc = torch.empty(len(grid), dtype=torch.float64, device=dev)
+    thr = torch.empty(len(grid), dtype=torch.float64, device=dev)
+    p = _lib.ptr
+    d_x = torch.from_numpy(np.ascontiguousarray(mat)).to(dev)     # held until the sync below
+    d_l = torch.from_numpy(lab.astype(np.uint8)).to(dev)
+    d_w = torch.tensor(grid, dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().hadis_tune_weights(p(d_x), p(d_l), mat.shape[0], mat.shape[1], p(d_w),
+                                              len(grid), int(lab.sum()), p(acc), p(thr),
+                                              _lib.stream_handle()), "tune_weights")
+    got = list(zip(acc.cpu().tolist(), thr.cpu().tolist()))
+    assert [list(x) for x in got] == d["per_vector"]
+
+
+def test_tune_weights_rejects_degenerate(gpu_device):
+    from paper_2509_00642_b200.router import RouterError, tune_weights_features
+    with pytest.raises(RouterError):
+        tune_weights_features(np.zeros((2, 8)), [0, 0])
