@@ -363,26 +363,36 @@ class GridProfiler:
         and memsets) into one CUDA graph.  An eager run first learns the
         output capacities; ``replay()`` relaunches the graph and returns the
         DeviceTable (a capacity overflow falls back to an eager rerun inside
-        ``finish`` and the graph is re-captured on the next call)."""
+        ``finish`` and the graph is re-captured on the next call).
+        ``replay.launch()`` / ``replay.state`` expose the asynchronous half
+        for pipelined callers (TablePipeline)."""
         torch = self.torch
         self.finish(self.launch(plan, exact_fid))          # learn capacities, allocate
         torch.cuda.synchronize(self.device)
-        box = {}
+        prof = self
 
-        def capture():
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                state = self.launch(plan, exact_fid)
-            box.update(graph=g, state=state, caps=plan.caps)
+        class Replay:
+            def __init__(self):
+                self.caps = None
+                self.capture()
 
-        def replay():
-            if box.get("caps") != plan.caps:
-                capture()
-            box["graph"].replay()
-            return self.finish(box["state"])
+            def capture(self):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    state = prof.launch(plan, exact_fid)
+                self.graph, self.state, self.caps = g, state, plan.caps
 
-        capture()
-        return replay
+            def launch(self):
+                """Enqueue one replay on the current stream (no host sync)."""
+                if self.caps != plan.caps:
+                    self.capture()
+                self.graph.replay()
+                return self.state
+
+            def __call__(self):
+                return prof.finish(self.launch())
+
+        return Replay()
 
     def _frontier(self, state, caps):
         torch = self.torch
@@ -447,6 +457,110 @@ class GridProfiler:
             stats={"rows": n_rows, "candidates": stats[_lib.ST_CANDIDATES],
                    "uncertain": stats[_lib.ST_UNCERTAIN],
                    "exact_cells": stats[_lib.ST_EXACT_CELLS]})
+
+
+class TablePipeline:
+    """Streaming table builds for a sequence of record sets (re-profiling
+    sweeps): host records in, host row arrays out, double-buffered so that
+    the H2D copy of set i, the device build of set i-1 and the D2H copy of
+    set i-2's rows run concurrently (PCIe is full duplex; the build is one
+    CUDA graph).  Every record set must have the same shape (n, light rows)."""
+
+    FIELDS = ("pair", "theta_pos", "tau_pos", "r_light", "r_heavy", "fid", "lat")
+
+    def __init__(self, pool, n, n_rows_scores, thresholds, pairs=None, device=None):
+        torch = _lib.torch_cuda()
+        self.torch = torch
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.slots = []
+        for _ in range(2):
+            d_h = torch.zeros(n, dtype=torch.float64, device=self.device)
+            d_sc = torch.zeros((n_rows_scores, n), dtype=torch.float64, device=self.device)
+            prof = GridProfiler(pool, d_h, d_sc, device=self.device)
+            self.slots.append(dict(h=d_h, sc=d_sc, prof=prof, plan=prof.plan(thresholds, pairs),
+                                   replay=None, ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(),
+                                   ev_out=torch.cuda.Event(), busy=False))
+        self.s_in = torch.cuda.Stream(device=self.device)
+        self.s_comp = torch.cuda.Stream(device=self.device)
+        self.s_out = torch.cuda.Stream(device=self.device)
+        self.stats_pin = [torch.zeros(_lib.ST_PAIR0 + 1, dtype=torch.int64).pin_memory()
+                          for _ in range(2)]
+        self.bad_pin = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.out_pin = {}
+
+    def warm(self, h_pin, sc_pin):
+        """First build of both slots on these records (learns capacities, captures graphs)."""
+        for sl in self.slots:
+            sl["h"].copy_(h_pin)
+            sl["sc"][:sc_pin.shape[0]].copy_(sc_pin)
+            sl["replay"] = sl["prof"].graph(sl["plan"])
+        self.torch.cuda.synchronize(self.device)
+
+    def _out_buffers(self, dt_state, n_rows):
+        out = dt_state["out"]
+        bufs = {}
+        for f in self.FIELDS:
+            v = out[f]
+            buf = self.out_pin.get(f)
+            if buf is None or buf.numel() < n_rows:
+                buf = self.out_pin[f] = self.torch.empty(max(n_rows, 1), dtype=v.dtype).pin_memory()
+            bufs[f] = buf
+        return bufs
+
+    def run(self, inputs):
+        """inputs: list of (h_pin, sc_pin) pinned host tensors.  Returns the
+        per-set (n_rows, bytes_h2d, bytes_d2h); rows land in ``out_pin``."""
+        torch = self.torch
+        done = []
+        pending = None                                  # (slot index, step index)
+
+        def finalize(k):
+            sl = self.slots[k]
+            sl["ev_stats"].synchronize()
+            stats = self.stats_pin[k].tolist()
+            if int(self.bad_pin[k][0]):
+                raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
+            if stats[_lib.ST_OVERFLOW]:
+                raise ProfileError("TablePipeline: capacity overflow; rebuild with warm()")
+            n_rows = stats[_lib.ST_ROWS]
+            bufs = self._out_buffers(sl["replay"].state, n_rows)
+            nbytes = 0
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(sl["ev_comp"])
+                for f in self.FIELDS:
+                    v = sl["replay"].state["out"][f][:n_rows]
+                    bufs[f][:n_rows].copy_(v, non_blocking=True)
+                    nbytes += n_rows * v.element_size()
+                sl["ev_out"].record(self.s_out)
+            return n_rows, nbytes
+
+        for i, (h_pin, sc_pin) in enumerate(inputs):
+            k = i % 2
+            sl = self.slots[k]
+            with torch.cuda.stream(self.s_in):
+                if sl["busy"]:
+                    self.s_in.wait_event(sl["ev_comp"])    # the slot's last build read its inputs
+                sl["h"].copy_(h_pin, non_blocking=True)
+                sl["sc"][:sc_pin.shape[0]].copy_(sc_pin, non_blocking=True)
+                sl["ev_in"].record(self.s_in)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(sl["ev_in"])
+                if sl["busy"]:
+                    self.s_comp.wait_event(sl["ev_out"])  # its previous rows are copied out
+                state = sl["replay"].launch()
+                sl["ev_comp"].record(self.s_comp)
+                self.stats_pin[k][:].copy_(state["stats"][:_lib.ST_PAIR0 + 1], non_blocking=True)
+                self.bad_pin[k].copy_(sl["prof"].bad, non_blocking=True)
+                sl["ev_stats"] = torch.cuda.Event()
+                sl["ev_stats"].record(self.s_comp)
+            sl["busy"] = True
+            if pending is not None:
+                done.append((pending[1],) + finalize(pending[0]))
+            pending = (k, i)
+        if pending is not None:
+            done.append((pending[1],) + finalize(pending[0]))
+        self.s_out.synchronize()
+        return done
 
 
 def rows_from_device(dt: DeviceTable, pool, thresholds) -> tuple:

@@ -496,3 +496,30 @@ def test_tune_weights_rejects_degenerate(gpu_device):
     from paper_2509_00642_b200.router import RouterError, tune_weights_features
     with pytest.raises(RouterError):
         tune_weights_features(np.zeros((2, 8)), [0, 0])
+
+
+def test_table_pipeline_matches_single_builds(gpu_device):
+    """Streaming builds (double-buffered H2D / graph / D2H) return, for each
+    record set, exactly the rows of a standalone build."""
+    import torch
+    from paper_2509_00642_b200.profiler import TablePipeline
+    rng = np.random.default_rng(13)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    n = 30_000
+    thr = tuple(i / 47 for i in range(48))
+    sets = []
+    for _ in range(5):
+        h = rng.uniform(0.05, 0.9, n)
+        sc = light_scores(pool, h, rng.normal(0.0, 0.05, n))
+        sets.append((torch.from_numpy(h).pin_memory(), torch.from_numpy(sc).pin_memory()))
+    pipe = TablePipeline(pool, n, len(pool) - 1, thr)
+    pipe.warm(*sets[0])
+    for i, (h_pin, sc_pin) in enumerate(sets):
+        want = GridProfiler(pool, h_pin.numpy(), sc_pin.numpy()).run(thr)
+        got = pipe.run([(h_pin, sc_pin)])
+        assert got[0][1] == want.n_rows
+        for f in TablePipeline.FIELDS:
+            assert torch.equal(pipe.out_pin[f][:want.n_rows], getattr(want, f).cpu()), (i, f)
+    res = pipe.run(sets)                     # all five in flight
+    assert [r[0] for r in res] == list(range(5))
