@@ -109,10 +109,16 @@ __device__ __forceinline__ int guided_bin_dense(const double* u, int U, const ui
 // Uniform grid u[i] = i / (U - 1) (rp.nonuniform == 0): g = trunc(x (U - 1)) is
 // within one of the answer, so two independent compares finish it
 // (u[g - 1] <= x always holds; u padded with +inf).
+// Away from a grid point (fractional part of x (U - 1) in (1e-9, 1 - 1e-9),
+// far beyond the ~1e-13 rounding of x (U - 1) and of u[g] = g / (U - 1)) the
+// answer is g + 1 for both strict and non-strict counts, with no table read.
 template <bool kLE>
 __device__ __forceinline__ int uniform_bin(const double* u, int U, double x) {
   if (x >= 0.0 && x <= 1.0) {
-    const int g = min(__double2int_rz(x * (double)(U - 1)), U - 1);
+    const double y = x * (double)(U - 1);
+    const int g = min(__double2int_rz(y), U - 1);
+    const double fr = y - (double)g;
+    if (fr > 1e-9 && fr < 1.0 - 1e-9) return g + 1;
     const double u0 = u[g], u1 = u[g + 1];
     return g + (kLE ? (u0 <= x) + (u1 <= x) : (u0 < x) + (u1 < x));
   }
