@@ -947,25 +947,69 @@ nobypass_kernel(Grid g, const PairConst* __restrict__ pcs, uint32_t* kept_bm, Un
     s_fid[t] = start ? eval_cell(g, pc, k, t).fid : INFINITY;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // sequential pass over groups (U <= 8192): group ids, representatives, prefix minima
-    int cur = 0;
-    double run = INFINITY;
-    int rep = 0;
-    for (int t = 0; t < g.U; ++t) {
-      if (s_start[t] >= 0) {
-        if (t > 0) { s_rep[cur] = rep; run = fmin(run, s_fid[cur]); }
-        cur = t;
-        rep = t;
-        s_pre[t] = run;
-      } else {
-        s_start[t] = cur;
-        if (g.first_pos[t] < g.first_pos[rep]) rep = t;
-      }
+  // block scans over t (each thread owns a contiguous chunk): exclusive
+  // prefix-min of the group fidelities, inclusive max of the group starts
+  {
+    __shared__ double w_min[kRowThreads / 32];
+    __shared__ int w_max[kRowThreads / 32];
+    const int per = (g.U + blockDim.x - 1) / blockDim.x;
+    const int t0 = threadIdx.x * per, t1 = min(g.U, t0 + per);
+    double cmin = INFINITY;
+    int cmax = -1;
+    for (int t = t0; t < t1; ++t) { cmin = fmin(cmin, s_fid[t]); cmax = max(cmax, s_start[t]); }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double imin = cmin;
+    int imax = cmax;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double om = __shfl_up_sync(0xffffffffu, imin, off);
+      const int ox = __shfl_up_sync(0xffffffffu, imax, off);
+      if (lane >= off) { imin = fmin(imin, om); imax = max(imax, ox); }
     }
-    s_rep[cur] = rep;
+    if (lane == 31) { w_min[warp] = imin; w_max[warp] = imax; }
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      double wm = lane < nw ? w_min[lane] : INFINITY;
+      int wx = lane < nw ? w_max[lane] : -1;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double om = __shfl_up_sync(0xffffffffu, wm, off);
+        const int ox = __shfl_up_sync(0xffffffffu, wx, off);
+        if (lane >= off) { wm = fmin(wm, om); wx = max(wx, ox); }
+      }
+      if (lane < nw) { w_min[lane] = wm; w_max[lane] = wx; }
+    }
+    __syncthreads();
+    // carry-in = everything before this thread's chunk
+    const double prev_min = __shfl_up_sync(0xffffffffu, imin, 1);
+    const int prev_max = __shfl_up_sync(0xffffffffu, imax, 1);
+    double run = lane > 0 ? prev_min : INFINITY;
+    int cur = lane > 0 ? prev_max : -1;
+    if (warp > 0) { run = fmin(run, w_min[warp - 1]); cur = max(cur, w_max[warp - 1]); }
+    __syncthreads();
+    for (int t = t0; t < t1; ++t) {
+      const double f = s_fid[t];
+      const int st = s_start[t];
+      if (st >= 0) { s_pre[t] = run; cur = st; }
+      run = fmin(run, f);
+      s_start[t] = cur;                           // now: the start of t's group
+    }
   }
   __syncthreads();
+  // group representative: the member with the smallest caller position
+  for (int t = threadIdx.x; t < g.U; t += blockDim.x)
+    if (s_start[t] == t) s_rep[t] = t;
+  __syncthreads();
+  if (!*g.sorted) {                               // unsorted caller grid (rare): sequential
+    if (threadIdx.x == 0) {
+      for (int t = 0; t < g.U; ++t) {
+        const int st = s_start[t];
+        if (g.first_pos[t] < g.first_pos[s_rep[st]]) s_rep[st] = t;
+      }
+    }
+    __syncthreads();
+  }
   for (int t = threadIdx.x; t < g.U; t += blockDim.x) {
     if (s_start[t] != t) continue;
     const double f = s_fid[t], m = s_pre[t];
