@@ -364,6 +364,8 @@ def run_ours(args, cfg):
                          "peak_kind": peak_kind,
                          "algorithmic_bytes": alg_bytes, "bytes_moved_by_design": moved,
                          "moved_gbs": moved / (ms_b * 1e-3) / 1e9 if ms_b > 0 else 0.0},
+            "stage_bandwidth": stage_bandwidth(n, L_g, plan, rows, hbm,
+                                               {"b3": ms_b, "k1": ms_k1, "k2": ms_k2}),
             "e2e": {"value": cfg.cells / (e2e_max * 1e-3), "unit": "configs/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max},
             "gpu_launches": int(launches),
@@ -386,6 +388,27 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def stage_bandwidth(n, L, plan, rows, hbm, ms):
+    """DRAM-side bytes each HBM-facing stage must move by design, over its CUDA-event
+    time (context for the roofline; K1 is shared-memory-atomic bound, the frontier
+    passes F1/F3/F6 work out of L2 and are issue/latency bound, not listed)."""
+    if plan is None:
+        return {}
+    quads = -(-L // 4)
+    hist = 12 * (plan.U + 1) ** 2 * plan.n_light
+    staged = {
+        "b3": (8 * n * (1 + L) + n * (8 + 8 * quads), "reads h + L score rows, writes hfix + quads"),
+        "k1": (n * (8 + 8 * quads) + hist, "reads hfix + quads, writes the row-prefixed histograms"),
+        "k2": (2 * hist, "column prefix: reads and writes every histogram cell"),
+    }
+    out = {}
+    for k, (b, what) in staged.items():
+        t = ms.get(k, 0.0)
+        gbs = b / (t * 1e-3) / 1e9 if t > 0 else 0.0
+        out[k] = {"bytes": b, "ms": t, "gbs": gbs, "frac_of_hbm": gbs / hbm, "what": what}
+    return out
 
 
 def measure_allocation(torch, dev, steps, cpu_points=1):
