@@ -290,150 +290,190 @@ __device__ __forceinline__ void write_out(int cnt, F&& store) {
 // B3: scatter.  Tile t covers records [t*kBkTile, (t+1)*kBkTile); thread i
 // owns records tile0 + 2*(j*kBkThreads + i) + {0, 1}, j < kBkPer/2, so each
 // warp load is one 512-byte 128-bit-per-lane transaction.
+struct ScatterSmem {
+  unsigned long long* st64;   // [kBkTile] hfix staged in row order
+  uint16_t* st16;             // [kQuad][kBkTile] tau-bins staged in row order (aliases st64)
+  uint32_t* gpos;             // [kBkTile] sorted slot -> global position
+  uint32_t* cnt;              // [kMaxBins] tile row counts, then local row offsets
+  uint32_t* gbase;            // [kMaxBins] global base of the tile's run in each row
+  uint32_t* guide_lt;
+  uint32_t* guide_le;
+  double* thr;                // [U + 2], +inf padded
+  int64_t* warp;              // [32]
+  uint32_t* tile_n;
+};
+
+// kFast: a full tile on a uniform grid (no bounds checks, no table search in
+// the common case) -- the hot path; the general instantiation handles the
+// last tile and guided grids.
+template <bool kVec, bool kFast>
+__device__ __forceinline__ void scatter_tile(const double* __restrict__ h,
+                                             const double* __restrict__ scores, int64_t n,
+                                             int n_light, int U, double hscale, int mode,
+                                             const RowPlan& rp, uint64_t* __restrict__ hfix_rows,
+                                             uint16_t* __restrict__ bs_rows, const ScatterSmem& sm,
+                                             int64_t t0, int tn) {
+  constexpr int kP = kBkPer / 2;
+  const int B1 = U + 1;
+  auto bin_h = [&](double x) {
+    return kFast ? uniform_bin<false>(sm.thr, U, x) : plan_bin<false>(mode, sm.thr, U, sm.guide_lt, x);
+  };
+  auto bin_s = [&](double x) {
+    return kFast ? uniform_bin<true>(sm.thr, U, x) : plan_bin<true>(mode, sm.thr, U, sm.guide_le, x);
+  };
+  for (int i = threadIdx.x; i < B1; i += blockDim.x) sm.cnt[i] = 0;
+  __syncthreads();
+  // 1. theta-row + local rank (ATOMS returns the rank within the tile's row)
+  uint32_t key[kBkPer];          // (row << 16) | rank, 0xffffffff = no record
+  uint64_t hf[kBkPer];
+#pragma unroll
+  for (int j = 0; j < kP; ++j) {
+    const int r = 2 * (j * kBkThreads + threadIdx.x);
+    double x0 = 0.0, x1 = 0.0;
+    if (kVec && (kFast || r + 1 < tn)) {
+      const double2 v = *reinterpret_cast<const double2*>(h + t0 + r);
+      x0 = v.x; x1 = v.y;
+    } else {
+      if (r < tn) x0 = h[t0 + r];
+      if (r + 1 < tn) x1 = h[t0 + r + 1];
+    }
+    const double xs[2] = {x0, x1};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (kFast || r + e < tn) {
+        const double x = xs[e];
+        const int b = bin_h(x);
+        const uint32_t rank = atomicAdd(&sm.cnt[b], 1u);
+        key[2 * j + e] = ((uint32_t)b << 16) | rank;
+        hf[2 * j + e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
+      } else {
+        key[2 * j + e] = 0xffffffffu;
+        hf[2 * j + e] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  // 2. local exclusive offsets + one global reservation per non-empty row
+  {
+    const int per = (B1 + blockDim.x - 1) / blockDim.x;
+    const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+    int64_t tsum = 0;
+    for (int i = i0; i < i1; ++i) tsum += sm.cnt[i];
+    int64_t total;
+    int64_t run = block_excl_scan(tsum, sm.warp, &total);
+    for (int i = i0; i < i1; ++i) {
+      const uint32_t c = sm.cnt[i];
+      sm.gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
+      sm.cnt[i] = (uint32_t)run;          // now the local row offsets
+      run += c;
+    }
+    if (threadIdx.x == 0) *sm.tile_n = (uint32_t)total;
+  }
+  __syncthreads();
+  // 3. sorted slot per record, its global position, hfix staged in row order
+#pragma unroll
+  for (int e = 0; e < kBkPer; ++e) {
+    if (kFast || key[e] != 0xffffffffu) {
+      const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
+      const uint32_t slot = sm.cnt[b] + rank;
+      sm.gpos[slot] = sm.gbase[b] + rank;
+      sm.st64[slot] = hf[e];
+      key[e] = slot;
+    }
+  }
+  __syncthreads();
+  const int cnt = kFast ? kBkTile : (int)*sm.tile_n;
+  write_out(cnt, [&](int i) { hfix_rows[sm.gpos[i]] = sm.st64[i]; });
+  // 4. per light model: tau-bins staged into row order, four models per
+  //    write-out (one 8-byte store per record and quad).  Model l+1's
+  //    scores are loaded while model l is binned (software pipelined).
+  auto load_scores = [&](int l, double* sv) {
+    const double* srow = scores + (int64_t)l * n + t0;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const int r = 2 * (j * kBkThreads + threadIdx.x);
+      if (kVec && (kFast || r + 1 < tn)) {
+        const double2 v = *reinterpret_cast<const double2*>(srow + r);
+        sv[2 * j] = v.x; sv[2 * j + 1] = v.y;
+      } else {
+        sv[2 * j] = r < tn ? srow[r] : 0.0;
+        sv[2 * j + 1] = r + 1 < tn ? srow[r + 1] : 0.0;
+      }
+    }
+  };
+  double sn[kBkPer];
+  if (n_light > 0) load_scores(0, sn);
+  for (int l = 0; l < n_light; ++l) {
+    double sv[kBkPer];
+#pragma unroll
+    for (int e = 0; e < kBkPer; ++e) sv[e] = sn[e];
+    if (l + 1 < n_light) load_scores(l + 1, sn);
+    const int qm = l % kQuad;
+    if (qm == 0) __syncthreads();      // previous quad (or hfix) fully written out
+    uint16_t* st = sm.st16 + qm * kBkTile;
+#pragma unroll
+    for (int e = 0; e < kBkPer; ++e)
+      if (kFast || key[e] != 0xffffffffu) st[key[e]] = (uint16_t)bin_s(sv[e]);
+    if (qm == kQuad - 1 || l == n_light - 1) {
+      __syncthreads();
+      ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * n;
+      const uint16_t* s16 = sm.st16;
+      write_out(cnt, [&](int i) {
+        orow[sm.gpos[i]] = make_ushort4(s16[i], qm >= 1 ? s16[kBkTile + i] : 0,
+                                        qm >= 2 ? s16[2 * kBkTile + i] : 0,
+                                        qm >= 3 ? s16[3 * kBkTile + i] : 0);
+      });
+    }
+  }
+  __syncthreads();
+}
+
+template <bool kVec>
+__device__ __noinline__ void scatter_tile_general(const double* __restrict__ h,
+                                                  const double* __restrict__ scores, int64_t n,
+                                                  int n_light, int U, double hscale, int mode,
+                                                  const RowPlan& rp, uint64_t* __restrict__ hfix_rows,
+                                                  uint16_t* __restrict__ bs_rows,
+                                                  const ScatterSmem& sm, int64_t t0, int tn) {
+  scatter_tile<kVec, false>(h, scores, n, n_light, U, hscale, mode, rp, hfix_rows, bs_rows, sm,
+                            t0, tn);
+}
+
 template <bool kVec>
 __global__ void __launch_bounds__(kBkThreads, 1)
 bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ scores, int64_t n,
                       int n_light, const double* __restrict__ thr, int U, double hscale,
                       RowPlan rp, uint64_t* __restrict__ hfix_rows, uint16_t* __restrict__ bs_rows) {
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* s_st64 = reinterpret_cast<unsigned long long*>(smem);  // [kBkTile]
-  uint16_t* s_st16 = reinterpret_cast<uint16_t*>(s_st64);                   // [kQuad][kBkTile]
-  uint32_t* s_gpos = reinterpret_cast<uint32_t*>(s_st64 + kBkTile);  // [kBkTile] sorted -> global
-  uint32_t* s_cnt = s_gpos + kBkTile;                          // [kMaxBins]
-  uint32_t* s_gbase = s_cnt + kMaxBins;                        // [kMaxBins]
-  uint32_t* s_guide_lt = s_gbase + kMaxBins;                   // [kGuide + 1]
-  uint32_t* s_guide_le = s_guide_lt + (kGuide + 2);            // [kGuide + 1]
-  double* s_thr = reinterpret_cast<double*>(s_guide_le + (kGuide + 2));   // [U]
   __shared__ int64_t s_warp[32];
   __shared__ uint32_t s_tile_n;
+  ScatterSmem sm;
+  sm.st64 = reinterpret_cast<unsigned long long*>(smem);
+  sm.st16 = reinterpret_cast<uint16_t*>(sm.st64);
+  sm.gpos = reinterpret_cast<uint32_t*>(sm.st64 + kBkTile);
+  sm.cnt = sm.gpos + kBkTile;
+  sm.gbase = sm.cnt + kMaxBins;
+  sm.guide_lt = sm.gbase + kMaxBins;
+  sm.guide_le = sm.guide_lt + (kGuide + 2);
+  sm.thr = reinterpret_cast<double*>(sm.guide_le + (kGuide + 2));
+  sm.warp = s_warp;
+  sm.tile_n = &s_tile_n;
   for (int i = threadIdx.x; i <= kGuide; i += blockDim.x) {
-    s_guide_lt[i] = rp.guide_lt[i];
-    s_guide_le[i] = rp.guide_le[i];
+    sm.guide_lt[i] = rp.guide_lt[i];
+    sm.guide_le[i] = rp.guide_le[i];
   }
-  for (int i = threadIdx.x; i < U + 2; i += blockDim.x) s_thr[i] = i < U ? thr[i] : INFINITY;
-  const int B1 = U + 1;
+  for (int i = threadIdx.x; i < U + 2; i += blockDim.x) sm.thr[i] = i < U ? thr[i] : INFINITY;
   const int64_t tiles = ceil_div(n, kBkTile);
   const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
-  constexpr int kP = kBkPer / 2;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t t0 = tile * kBkTile;
     const int tn = (int)min((int64_t)kBkTile, n - t0);
-    for (int i = threadIdx.x; i < B1; i += blockDim.x) s_cnt[i] = 0;
-    __syncthreads();
-    // 1. bin + local rank (ATOMS returns the rank within the tile's row)
-    uint32_t key[kBkPer];          // (row << 16) | rank, 0xffffffff = no record
-    uint64_t hf[kBkPer];
-#pragma unroll
-    for (int j = 0; j < kP; ++j) {
-      const int r = 2 * (j * kBkThreads + threadIdx.x);
-      double x0 = 0.0, x1 = 0.0;
-      if (kVec && r + 1 < tn) {
-        const double2 v = *reinterpret_cast<const double2*>(h + t0 + r);
-        x0 = v.x; x1 = v.y;
-      } else {
-        if (r < tn) x0 = h[t0 + r];
-        if (r + 1 < tn) x1 = h[t0 + r + 1];
-      }
-      const double xs[2] = {x0, x1};
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (r + e < tn) {
-          const double x = xs[e];
-          const int b = plan_bin<false>(mode, s_thr, U, s_guide_lt, x);
-          const uint32_t rank = atomicAdd(&s_cnt[b], 1u);
-          key[2 * j + e] = ((uint32_t)b << 16) | rank;
-          hf[2 * j + e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
-        } else {
-          key[2 * j + e] = 0xffffffffu;
-          hf[2 * j + e] = 0;
-        }
-      }
-    }
-    __syncthreads();
-    // 2. local exclusive offsets + one global reservation per non-empty row
-    {
-      const int per = (B1 + blockDim.x - 1) / blockDim.x;
-      const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
-      int64_t tsum = 0;
-      for (int i = i0; i < i1; ++i) tsum += s_cnt[i];
-      int64_t total;
-      int64_t run = block_excl_scan(tsum, s_warp, &total);
-      for (int i = i0; i < i1; ++i) {
-        const uint32_t c = s_cnt[i];
-        s_gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
-        s_cnt[i] = (uint32_t)run;          // s_cnt now holds the local row offsets
-        run += c;
-      }
-      if (threadIdx.x == 0) s_tile_n = (uint32_t)total;
-    }
-    __syncthreads();
-    // 3. sorted slot per record; global position per slot; hfix low half
-#pragma unroll
-    for (int e = 0; e < kBkPer; ++e) {
-      if (key[e] != 0xffffffffu) {
-        const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
-        const uint32_t slot = s_cnt[b] + rank;
-        s_gpos[slot] = s_gbase[b] + rank;
-        s_st64[slot] = hf[e];
-        key[e] = slot;
-      }
-    }
-    __syncthreads();
-    const int cnt = (int)s_tile_n;
-    write_out(cnt, [&](int i) { hfix_rows[s_gpos[i]] = s_st64[i]; });
-    // 4. per light model: tau-bins staged into row order, four models per
-    //    write-out (one 8-byte store per record and quad).  Model l+1's
-    //    scores are loaded while model l is binned (software pipelined).
-    auto load_scores = [&](int l, double* sv) {
-      const double* srow = scores + (int64_t)l * n + t0;
-#pragma unroll
-      for (int j = 0; j < kP; ++j) {
-        const int r = 2 * (j * kBkThreads + threadIdx.x);
-        if (kVec && r + 1 < tn) {
-          const double2 v = *reinterpret_cast<const double2*>(srow + r);
-          sv[2 * j] = v.x; sv[2 * j + 1] = v.y;
-        } else {
-          sv[2 * j] = r < tn ? srow[r] : 0.0;
-          sv[2 * j + 1] = r + 1 < tn ? srow[r + 1] : 0.0;
-        }
-      }
-    };
-    double sn[kBkPer];
-    if (n_light > 0) load_scores(0, sn);
-    for (int l = 0; l < n_light; ++l) {
-      double sv[kBkPer];
-#pragma unroll
-      for (int e = 0; e < kBkPer; ++e) sv[e] = sn[e];
-      if (l + 1 < n_light) load_scores(l + 1, sn);
-      const int qm = l % kQuad;
-      if (qm == 0) __syncthreads();      // previous quad (or hfix) fully written out
-      uint16_t* st = s_st16 + qm * kBkTile;
-      if (mode == 0) {
-#pragma unroll
-        for (int e = 0; e < kBkPer; ++e)
-          if (key[e] != 0xffffffffu) st[key[e]] = (uint16_t)uniform_bin<true>(s_thr, U, sv[e]);
-      } else if (mode == 1) {
-#pragma unroll
-        for (int e = 0; e < kBkPer; ++e)
-          if (key[e] != 0xffffffffu)
-            st[key[e]] = (uint16_t)guided_bin_dense<true>(s_thr, U, s_guide_le, sv[e]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < kBkPer; ++e)
-          if (key[e] != 0xffffffffu)
-            st[key[e]] = (uint16_t)guided_bin<true>(s_thr, U, s_guide_le, sv[e]);
-      }
-      if (qm == kQuad - 1 || l == n_light - 1) {
-        __syncthreads();
-        ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * n;
-        write_out(cnt, [&](int i) {
-          orow[s_gpos[i]] = make_ushort4(s_st16[i], qm >= 1 ? s_st16[kBkTile + i] : 0,
-                                         qm >= 2 ? s_st16[2 * kBkTile + i] : 0,
-                                         qm >= 3 ? s_st16[3 * kBkTile + i] : 0);
-        });
-      }
-    }
-    __syncthreads();
+    if (mode == 0 && tn == kBkTile)
+      scatter_tile<kVec, true>(h, scores, n, n_light, U, hscale, mode, rp, hfix_rows, bs_rows, sm,
+                               t0, tn);
+    else
+      scatter_tile_general<kVec>(h, scores, n, n_light, U, hscale, mode, rp, hfix_rows, bs_rows,
+                                 sm, t0, tn);
   }
 }
 
