@@ -534,8 +534,6 @@ row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs
                 int n_light, RowPlan rp, uint32_t* __restrict__ g_cnt,
                 unsigned long long* __restrict__ g_hsum, uint8_t* __restrict__ row_scanned) {
   extern __shared__ __align__(16) uint32_t s_bin[];    // [kQuad][4][B1s]
-  __shared__ uint32_t ws_c[kK1Threads / 32];
-  __shared__ unsigned long long ws_h[kK1Threads / 32];
   const int B1 = U + 1;
   const int B1s = B1 | 1;                               // odd stride between limb arrays
   const int64_t items = rp.item_off[U + 1];
@@ -558,20 +556,20 @@ row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs
   if (narrow) row_accumulate<true>(hf, bq, r0, r1, base, nm, s_bin, B1s);
   else row_accumulate<false>(hf, bq, r0, r1, base, nm, s_bin, B1s);
   __syncthreads();
-  for (int m = 0; m < nm; ++m) {
-    const int l = quad * kQuad + m;
-    const uint32_t* sb = s_bin + m * 4 * B1s;
-    uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
-    unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
-    auto bin_sum = [&](int i) {
-      return (unsigned long long)sb[i] * base + (unsigned long long)sb[B1s + i] +
-             ((unsigned long long)sb[2 * B1s + i] << 16) +
-             (narrow ? 0ull : (unsigned long long)sb[3 * B1s + i] << 32);
-    };
-    if (!whole_row || !row_scanned) {
+  auto bin_sum = [&](const uint32_t* sb, int i) {
+    return (unsigned long long)sb[i] * base + (unsigned long long)sb[B1s + i] +
+           ((unsigned long long)sb[2 * B1s + i] << 16) +
+           (narrow ? 0ull : (unsigned long long)sb[3 * B1s + i] << 32);
+  };
+  if (!whole_row || !row_scanned) {
+    for (int m = 0; m < nm; ++m) {
+      const int l = quad * kQuad + m;
+      const uint32_t* sb = s_bin + m * 4 * B1s;
+      uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
+      unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
       for (int i = threadIdx.x; i < B1; i += blockDim.x) {
         const uint32_t c = sb[i];
-        const unsigned long long v = bin_sum(i);
+        const unsigned long long v = bin_sum(sb, i);
         if (whole_row) {
           gc[i] = c;
           gh[i] = v;
@@ -580,49 +578,72 @@ row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs
           atomicAdd(&gh[i], v);
         }
       }
-      continue;
     }
-    // whole row: emit the K2 row prefix (along bs) directly -- thread-contiguous
-    // segments, block scan of the segment totals, then the segment prefixes
-    const int per = (B1 + blockDim.x - 1) / blockDim.x;
-    const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
-    uint32_t tc = 0;
-    unsigned long long th = 0;
-    for (int i = i0; i < i1; ++i) { tc += sb[i]; th += bin_sum(i); }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t ic = tc;
-    unsigned long long ih = th;
+    return;
+  }
+  // whole row: emit the K2 row prefix (along bs) of all nm models at once --
+  // thread-contiguous segments, one block scan of the segment totals (per
+  // model, carried together), then the segment prefixes
+  const int per = (B1 + blockDim.x - 1) / blockDim.x;
+  const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+  uint32_t tc[kQuad];
+  unsigned long long th[kQuad];
+#pragma unroll
+  for (int m = 0; m < kQuad; ++m) {
+    tc[m] = 0;
+    th[m] = 0;
+    if (m < nm)
+      for (int i = i0; i < i1; ++i) { tc[m] += s_bin[m * 4 * B1s + i]; th[m] += bin_sum(s_bin + m * 4 * B1s, i); }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t ic[kQuad];
+  unsigned long long ih[kQuad];
+#pragma unroll
+  for (int m = 0; m < kQuad; ++m) { ic[m] = tc[m]; ih[m] = th[m]; }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+    for (int m = 0; m < kQuad; ++m) {
+      const uint32_t oc = __shfl_up_sync(0xffffffffu, ic[m], off);
+      const unsigned long long oh = __shfl_up_sync(0xffffffffu, ih[m], off);
+      if (lane >= off) { ic[m] += oc; ih[m] += oh; }
+    }
+  }
+  __shared__ uint32_t ws_cq[kQuad][kK1Threads / 32];
+  __shared__ unsigned long long ws_hq[kQuad][kK1Threads / 32];
+  if (lane == 31)
+#pragma unroll
+    for (int m = 0; m < kQuad; ++m) { ws_cq[m][warp] = ic[m]; ws_hq[m][warp] = ih[m]; }
+  __syncthreads();
+  if (warp < kQuad) {
+    const int m = warp, nw = blockDim.x >> 5;
+    uint32_t wc = lane < nw ? ws_cq[m][lane] : 0u;
+    unsigned long long wh = lane < nw ? ws_hq[m][lane] : 0ull;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, off);
-      const unsigned long long oh = __shfl_up_sync(0xffffffffu, ih, off);
-      if (lane >= off) { ic += oc; ih += oh; }
+      const uint32_t oc = __shfl_up_sync(0xffffffffu, wc, off);
+      const unsigned long long oh = __shfl_up_sync(0xffffffffu, wh, off);
+      if (lane >= off) { wc += oc; wh += oh; }
     }
-    if (lane == 31) { ws_c[warp] = ic; ws_h[warp] = ih; }
-    __syncthreads();
-    if (warp == 0) {
-      const int nw = blockDim.x >> 5;
-      uint32_t wc = lane < nw ? ws_c[lane] : 0u;
-      unsigned long long wh = lane < nw ? ws_h[lane] : 0ull;
+    if (lane < nw) { ws_cq[m][lane] = wc; ws_hq[m][lane] = wh; }
+  }
+  __syncthreads();
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t oc = __shfl_up_sync(0xffffffffu, wc, off);
-        const unsigned long long oh = __shfl_up_sync(0xffffffffu, wh, off);
-        if (lane >= off) { wc += oc; wh += oh; }
-      }
-      if (lane < nw) { ws_c[lane] = wc; ws_h[lane] = wh; }
-    }
-    __syncthreads();
-    uint32_t rc = (warp > 0 ? ws_c[warp - 1] : 0u) + ic - tc;
-    unsigned long long rh = (warp > 0 ? ws_h[warp - 1] : 0ull) + ih - th;
+  for (int m = 0; m < kQuad; ++m) {
+    if (m >= nm) break;
+    const int l = quad * kQuad + m;
+    const uint32_t* sb = s_bin + m * 4 * B1s;
+    uint32_t* gc = g_cnt + ((int64_t)l * B1 + k) * B1;
+    unsigned long long* gh = g_hsum + ((int64_t)l * B1 + k) * B1;
+    uint32_t rc = (warp > 0 ? ws_cq[m][warp - 1] : 0u) + ic[m] - tc[m];
+    unsigned long long rh = (warp > 0 ? ws_hq[m][warp - 1] : 0ull) + ih[m] - th[m];
     for (int i = i0; i < i1; ++i) {
       rc += sb[i];
-      rh += bin_sum(i);
+      rh += bin_sum(sb, i);
       gc[i] = rc;
       gh[i] = rh;
     }
     if (threadIdx.x == 0) row_scanned[(int64_t)l * B1 + k] = 1;
-    __syncthreads();                                   // ws_c / ws_h reuse
   }
 }
 
