@@ -40,7 +40,7 @@ struct PairConst {
   double Ll, Lh, bl, pl, bh, ph;
   double delta2;       // 2 * delta (fidelity space)
   double delta2_S;     // the same margin in numerator space (fid* * n), padded
-  double lo_x, scale_x;  // latency-numerator bucket map: b = floor((x - lo_x) * scale_x)
+  double off_x, scale_x;  // latency-numerator bucket map: b = floor(fma(x, scale_x, off_x))
   int slot;
 };
 
@@ -74,14 +74,15 @@ __device__ __forceinline__ const uint64_t* slot_hs(const Grid& g, int slot) {
 }
 
 // fid* numerator, the one formula every stage uses (so equal heavy sets give
-// bitwise-equal values):  S = (b_h nH + p_h SH 2^-s) + (b_l nL + p_l SL 2^-s).
+// bitwise-equal values):  S = p_h SH 2^-s + (b_h nH + (p_l SL 2^-s + b_l nL)),
+// each + a fused multiply-add (two FP64 pipe ops per heavy partner).
 // The light part depends on the light model only, so row passes stage it
 // once per cell for all heavy partners.  SH 2^-s is exact (power of two).
 __device__ __forceinline__ double light_part(double bl, double pl, double dnL, double dSLs) {
-  return __dadd_rn(__dmul_rn(bl, dnL), __dmul_rn(pl, dSLs));
+  return __fma_rn(pl, dSLs, __dmul_rn(bl, dnL));
 }
 __device__ __forceinline__ double fid_num(double bh, double ph, double dnH, double dSHs, double lp) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(bh, dnH), __dmul_rn(ph, dSHs)), lp);
+  return __fma_rn(ph, dSHs, __fma_rn(bh, dnH, lp));
 }
 
 __device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc, int k, int t) {
@@ -159,13 +160,17 @@ __device__ __forceinline__ void numerators_of(const Grid& g, const PairConst& pc
 // bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
 __device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, double x) {
   // floor + saturating convert in one instruction (NaN -> INT_MIN -> bucket 0)
-  const int b = __double2int_rd(__dmul_rn(__dadd_rn(x, -pc.lo_x), pc.scale_x));
+  const int b = __double2int_rd(__fma_rn(x, pc.scale_x, pc.off_x));
   return min(max(b, 0), nbuckets - 1);
 }
 
-// order_key without branches (same map as common.cuh's order_key)
+// min of two non-NaN doubles: one FP64-pipe compare + two selects
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+// order_key without branches and without folding -0.0 into +0.0: row passes
+// only use these keys for minima / value compares, where -0 < +0 is harmless
 __device__ __forceinline__ unsigned long long order_key_fast(double x) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(__dadd_rn(x, 0.0));
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
   return b ^ ((unsigned long long)((long long)b >> 63) | 0x8000000000000000ull);
 }
 
@@ -254,8 +259,8 @@ __global__ void pair_const_kernel(int n_pairs, const int32_t* __restrict__ pair_
   c.delta2_S = c.delta2 * dn * 1.001;
   const double lo = fmin(c.Ll, c.Lh) * dn * (1.0 - 1e-12);
   const double hi = (c.Ll + c.Lh) * dn * (1.0 + 1e-12);
-  c.lo_x = lo;
   c.scale_x = (double)nbuckets / (hi - lo);
+  c.off_x = -lo * c.scale_x;
   out[p] = c;
 }
 
@@ -345,7 +350,7 @@ struct RowSmem {
   double SHs[kRowWarps][kRowT * kRowPad];   // their hardness sum * 2^-shift
   double LP[kRowWarps][kRowT * kRowPad];    // light part of the fid* numerator
   uint8_t cls[kRowWarps][kRowT * kRowPad];  // 1 = first of its duplicate run, 2 = past the end
-  unsigned long long carry[kRowWarps][kMaxGroup];
+  double carry[kRowWarps][kMaxGroup];
   PairConst pc[kMaxGroup];
 };
 
@@ -365,9 +370,10 @@ __device__ __forceinline__ bool row_task(const Grid& g, const PairConst* __restr
   return *k < g.U && g.row_start[*k];
 }
 
-// visit(p, pc, w0, key[kRowT], take) once per (window, partner), all lanes:
-// lane l owns cells t = w0 + l*kRowT + j; key[j] = order_key(S) (S = +inf past
-// the row end); bit j of take = the cell passes the row test -- strict
+// visit(p, pc, w0, sv[kRowT], take) once per (window, partner), all lanes:
+// lane l owns cells t = w0 + l*kRowT + j; sv[j] = S (+inf past the row end;
+// minima and compares run on the FP64 pipe, which has the slack -- u64 keys
+// cost four ALU ops per min); bit j of take = the cell passes the row test -- strict
 // prefix-min (F1) or class start within 2 delta of the prefix-min (F3).
 template <bool kFilter, typename F>
 __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0, int p1, int k,
@@ -387,7 +393,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
   uint8_t* s_cls = sm.cls[warp];
   {
     const int q0 = p0, q1 = p1;
-    for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = ~0ull;
+    for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = INFINITY;
     for (int w0 = 0; w0 < g.U; w0 += kRowWin) {
       __syncwarp();
       // stage: all kRowT coalesced loads of the window in flight, then convert
@@ -423,44 +429,51 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         }
       }
       __syncwarp();
-      for (int p = q0; p < q1; ++p) {
+      // one partner: S of the lane's cells, warp scan of the lane minima (the
+      // row carry enters through lane 0, so only lane 0 touches it), row test
+      auto scan = [&](int p, double (&sv)[kRowT]) -> unsigned {
         const PairConst& pc = sm.pc[p - p0];
         const double ph = pc.ph, bh = pc.bh;
-        unsigned long long key[kRowT];
-        unsigned long long lmin = ~0ull;
+        double lmin = INFINITY;
 #pragma unroll
         for (int j = 0; j < kRowT; ++j) {
           const int at = j * kRowPad + lane;
-          key[j] = order_key_fast(fid_num(bh, ph, s_nH[at], s_SHs[at], s_LP[at]));
-          lmin = min(lmin, key[j]);
+          sv[j] = fid_num(bh, ph, s_nH[at], s_SHs[at], s_LP[at]);
+          lmin = dmin(lmin, sv[j]);
         }
-        unsigned long long incl = lmin;
+        double* const carry = &sm.carry[warp][p - q0];
+        const double c0 = lane == 0 ? *carry : INFINITY;
+        double incl = dmin(lmin, c0);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-          const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl = min(incl, o);
+          const double o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl = dmin(incl, o);
         }
-        unsigned long long run = __shfl_up_sync(0xffffffffu, incl, 1);
-        const unsigned long long carry = sm.carry[warp][p - q0];
-        run = lane == 0 ? carry : min(carry, run);
-        const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-        if (lane == 0) sm.carry[warp][p - q0] = min(carry, tot);
+        double run = __shfl_up_sync(0xffffffffu, incl, 1);
+        const double tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) {
+          run = c0;
+          *carry = tot;
+        }
         unsigned take = 0;
         const double dpc = pc.delta2_S;
 #pragma unroll
         for (int j = 0; j < kRowT; ++j) {
           bool t_ok;
           if (kFilter) {
-            const double rowmin = run == ~0ull ? INFINITY : from_order_key(run);
-            t_ok = s_cls[j * kRowPad + lane] == 1 && from_order_key(key[j]) <= rowmin + dpc;
+            t_ok = s_cls[j * kRowPad + lane] == 1 && sv[j] <= run + dpc;
           } else {
-            t_ok = key[j] < run;
+            t_ok = sv[j] < run;
           }
           take |= (unsigned)t_ok << j;
-          run = min(run, key[j]);
+          run = dmin(run, sv[j]);
         }
-        visit(p, pc, w0, key, take);
+        return take;
+      };
+      for (int p = q0; p < q1; ++p) {
+        double sv[kRowT];
+        const unsigned take = scan(p, sv);
+        visit(p, sm.pc[p - p0], w0, sv, take);
       }
     }
     __syncwarp();
@@ -483,15 +496,18 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
   const double dRk = (double)slot_cnt(g, sm.pc[0].slot)[(int64_t)k * g.B1 + g.U];
   const double* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
-                                            const unsigned long long* key, unsigned take) {
+                                            const double* sv, unsigned take) {
     unsigned long long* const bp = bmin + (int64_t)p * (g.nbuckets >> kCoarseShift);
     const double xr = __dmul_rn(dRk, pc.Ll);
     int bk[kRowT];
     unsigned long long cur[kRowT];
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j)
-      bk[j] = bucket_of_x(pc, g.nbuckets,
-                          __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh))) >> kCoarseShift;
+    for (int j = 0; j < kRowT; ++j)                // only taken cells need a bucket
+      bk[j] = (take >> j & 1u)
+                  ? bucket_of_x(pc, g.nbuckets,
+                                __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh))) >>
+                        kCoarseShift
+                  : -1 - j;
     // row-frontier keys strictly decrease along the walk: of consecutive taken
     // cells in one coarse bucket only the last can lower its minimum
 #pragma unroll
@@ -500,8 +516,10 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
 #pragma unroll
     for (int j = 0; j < kRowT; ++j) cur[j] = (take >> j & 1u) ? bp[bk[j]] : 0ull;
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j)
-      if (key[j] < cur[j]) atomicMin(bp + bk[j], key[j]);
+    for (int j = 0; j < kRowT; ++j) {
+      const unsigned long long key = order_key_fast(sv[j]);
+      if ((take >> j & 1u) && key < cur[j]) atomicMin(bp + bk[j], key);
+    }
   });
 }
 
@@ -800,19 +818,21 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
   const double* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
-                                           const unsigned long long* key, unsigned take) {
+                                           const double* sv, unsigned take) {
     const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
     const double xr = __dmul_rn(dRk, pc.Ll);
     int bk[kRowT];
     double gv[kRowT];
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j)
-      bk[j] = bucket_of_x(pc, g.nbuckets, __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)));
+    for (int j = 0; j < kRowT; ++j)                // only cells passing the row test
+      bk[j] = (take >> j & 1u) ? bucket_of_x(pc, g.nbuckets,
+                                             __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)))
+                               : 0;
 #pragma unroll
     for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j] >> kCoarseShift] : -INFINITY;
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)
-      if (!(from_order_key(key[j]) <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
+      if (!(sv[j] <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
     // one list reservation per (window, partner)
     const int cnt = __popc(take);
     int incl = cnt;
@@ -836,7 +856,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
         lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
                          (uint32_t)bk[j], 0u,
                          __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)),
-                         from_order_key(key[j])};
+                         sv[j]};
       }
       ++at;
     }
