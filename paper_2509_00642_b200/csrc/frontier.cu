@@ -164,6 +164,11 @@ __device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, do
   return min(max(b, 0), nbuckets - 1);
 }
 
+// exact u32 -> f64 on the FP64 pipe (I2F runs on the 4x slower XU pipe)
+__device__ __forceinline__ double u32_to_double(uint32_t v) {
+  return __dadd_rn(__hiloint2double(0x43300000, (int)v), -4503599627370496.0);
+}
+
 // min of two non-NaN doubles: one FP64-pipe compare + two selects
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 
@@ -340,13 +345,14 @@ struct Cands {
 // skipped.
 constexpr int kRowWarps = 8;
 constexpr int kCoarseShift = 4;      // F1/F3 latency buckets: the fine ones >> 4
+                                     // (3 and 5 measured: F1 vs candidate trade-off, no gain)
 constexpr int kMaxGroup = 64;        // heavy partners per light slot (pool <= 65 models)
 constexpr int kRowT = 8;             // cells per lane per window
 constexpr int kRowWin = 32 * kRowT;  // cells per window
 constexpr int kRowPad = 33;
 
 struct RowSmem {
-  double nH[kRowWarps][kRowT * kRowPad];    // heavy-served records
+  uint32_t nH[kRowWarps][kRowT * kRowPad];  // heavy-served records (u32: 4 CTAs/SM fit)
   double SHs[kRowWarps][kRowT * kRowPad];   // their hardness sum * 2^-shift
   double LP[kRowWarps][kRowT * kRowPad];    // light part of the fid* numerator
   uint8_t cls[kRowWarps][kRowT * kRowPad];  // 1 = first of its duplicate run, 2 = past the end
@@ -387,7 +393,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
   const uint64_t Htot = Sh[(int64_t)g.U * g.B1 + g.U];
   const uint64_t Hnb = Htot - Sh[rk + g.U];        // hardness of bypassed records
   const double bl = sm.pc[0].bl, pl = sm.pc[0].pl, inv = g.inv_scale;
-  double* s_nH = sm.nH[warp];
+  uint32_t* s_nH = sm.nH[warp];
   double* s_SHs = sm.SHs[warp];
   double* s_LP = sm.LP[warp];
   uint8_t* s_cls = sm.cls[warp];
@@ -417,12 +423,12 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
           const uint32_t nr = nrv[r];
           const uint64_t SH = Hnb + shv[r];
           const uint32_t nH = (n - Rk) + nr;
-          s_nH[at] = (double)nH;
+          s_nH[at] = nH;
           s_SHs[at] = __dmul_rn((double)SH, inv);
           s_LP[at] = light_part(bl, pl, (double)(n - nH), __dmul_rn((double)(Htot - SH), inv));
           s_cls[at] = t == 0 || nr != left;
         } else {                                         // past the row end: S = +inf
-          s_nH[at] = 0.0;
+          s_nH[at] = 0u;
           s_SHs[at] = 0.0;
           s_LP[at] = INFINITY;
           s_cls[at] = 2;
@@ -438,7 +444,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 #pragma unroll
         for (int j = 0; j < kRowT; ++j) {
           const int at = j * kRowPad + lane;
-          sv[j] = fid_num(bh, ph, s_nH[at], s_SHs[at], s_LP[at]);
+          sv[j] = fid_num(bh, ph, u32_to_double(s_nH[at]), s_SHs[at], s_LP[at]);
           lmin = dmin(lmin, sv[j]);
         }
         double* const carry = &sm.carry[warp][p - q0];
@@ -485,7 +491,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 // dominated by an earlier cell of its row, which sits in the same or a lower
 // bucket).  Reads the current minima first (all in flight): most cells do
 // not lower them.
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, 4)
 bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
                   const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -494,7 +500,7 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
   if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k)) return;
   const int lane = threadIdx.x & 31;
   const double dRk = (double)slot_cnt(g, sm.pc[0].slot)[(int64_t)k * g.B1 + g.U];
-  const double* s_nH = sm.nH[threadIdx.x >> 5];
+  const uint32_t* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
                                             const double* sv, unsigned take) {
     unsigned long long* const bp = bmin + (int64_t)p * (g.nbuckets >> kCoarseShift);
@@ -505,7 +511,7 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
     for (int j = 0; j < kRowT; ++j)                // only taken cells need a bucket
       bk[j] = (take >> j & 1u)
                   ? bucket_of_x(pc, g.nbuckets,
-                                __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh))) >>
+                                __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh))) >>
                         kCoarseShift
                   : -1 - j;
     // row-frontier keys strictly decrease along the walk: of consecutive taken
@@ -802,7 +808,7 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
 // They are appended to an unordered list (one atomic per warp and partner)
 // and counted per (pair, bucket); F5 then groups them by bucket.
 
-__global__ void __launch_bounds__(kRowWarps * 32)
+__global__ void __launch_bounds__(kRowWarps * 32, 3)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
               uint32_t* __restrict__ bcnt, Cands lst, int64_t cap,
@@ -816,7 +822,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const uint32_t krep = (uint32_t)g.row_rep[k] * (uint32_t)g.U;
   const bool sorted_thr = *g.sorted != 0;          // first_pos increasing: rep = own rank
   const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
-  const double* s_nH = sm.nH[threadIdx.x >> 5];
+  const uint32_t* s_nH = sm.nH[threadIdx.x >> 5];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
                                            const double* sv, unsigned take) {
     const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
@@ -826,7 +832,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)                // only cells passing the row test
       bk[j] = (take >> j & 1u) ? bucket_of_x(pc, g.nbuckets,
-                                             __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)))
+                                             __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh)))
                                : 0;
 #pragma unroll
     for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j] >> kCoarseShift] : -INFINITY;
@@ -855,7 +861,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
         const int t = w0 + lane * kRowT + j;
         lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
                          (uint32_t)bk[j], 0u,
-                         __dadd_rn(xr, __dmul_rn(s_nH[j * kRowPad + lane], pc.Lh)),
+                         __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh)),
                          sv[j]};
       }
       ++at;
