@@ -1358,7 +1358,7 @@ emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __re
     const int64_t c = s_cell[i];
     const int64_t r = (int64_t)base + i;
     if (c >= cells || r >= out_cap) continue;
-    const int k = (int)(c / g.U), t = (int)(c % g.U);
+    const int k = (int)((uint32_t)c / (uint32_t)g.U), t = (int)((uint32_t)c - (uint32_t)k * g.U);
     const CellVal v = eval_cell(g, pc, k, t);
     out.pair[r] = p;
     out.theta_pos[r] = g.first_pos[k];

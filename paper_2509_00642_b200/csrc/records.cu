@@ -37,8 +37,8 @@ constexpr int kGuide = 4096;          // guide buckets over [0, 1]
 constexpr int kMaxBins = 2048;        // U + 1 <= kMaxBins (u16 bins)
 constexpr int kRowChunk = 32768;      // records per K1 CTA: 2^15 * 2^16 < 2^31 per limb
 constexpr int kK1Threads = 512;
-constexpr int kBkThreads = 1024;      // scatter CTA
-constexpr int kBkTile = 8192;         // records per scatter tile
+constexpr int kBkThreads = 1024;      // scatter CTA (512 x 2/SM and 4096-record tiles: slower;
+constexpr int kBkTile = 8192;         // records per scatter tile   L2 bulk prefetch ahead: slower)
 constexpr int kBkPer = kBkTile / kBkThreads;   // records per thread per tile (even)
 constexpr int kCountThreads = 512;
 

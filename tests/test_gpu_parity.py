@@ -523,3 +523,57 @@ def test_table_pipeline_matches_single_builds(gpu_device):
             assert torch.equal(pipe.out_pin[f][:want.n_rows], getattr(want, f).cpu()), (i, f)
     res = pipe.run(sets)                     # all five in flight
     assert [r[0] for r in res] == list(range(5))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_scale_properties(gpu_device, name):
+    """BASELINE c3 / c4 at full size (8 / 16 models, 10M records, 512^2 / 1024^2 grid):
+    per-pair (theta, tau) order, no table row dominated by another (theta = max
+    rows excepted, profiler.py:168-173), and on sampled cells, numpy's
+    profiler.py:146-165 arithmetic: table rows match it (bit-exact counts and
+    latency, fid 1e-9) and cells outside the table are weakly dominated by a row."""
+    from paper_2509_00642_b200 import synth
+    cfg = synth.CONFIGS[name]
+    pool, h, noise, scores = synth.records(cfg)
+    thr = cfg.thresholds
+    dt = GridProfiler(pool, h, scores).run(thr)
+    assert dt.n_rows > 0 and len(dt.pairs) == cfg.n_pairs
+    pair = dt.pair.cpu().numpy()
+    tp, cp = dt.theta_pos.cpu().numpy(), dt.tau_pos.cpu().numpy()
+    lat, fid = dt.lat.cpu().numpy(), dt.fid.cpu().numpy()
+    rl, rh = dt.r_light.cpu().numpy(), dt.r_heavy.cpu().numpy()
+    K = len(thr)
+    assert np.all(np.diff(pair) >= 0)
+    starts = np.searchsorted(pair, np.arange(len(dt.pairs) + 1))
+    for p in range(len(dt.pairs)):
+        a, b = starts[p], starts[p + 1]
+        assert b > a
+        key = tp[a:b].astype(np.int64) * K + cp[a:b]
+        assert np.all(np.diff(key) > 0)                     # (theta, tau) order, no duplicates
+        o = np.lexsort((fid[a:b], lat[a:b]))
+        f = fid[a:b][o]
+        prev_min = np.minimum.accumulate(np.concatenate(([np.inf], f[:-1])))
+        free = np.asarray(thr)[tp[a:b][o]] != max(thr)
+        assert np.all(f[free] < prev_min[free])              # strictly below all cheaper rows
+    rng = random.Random(4)
+    for _ in range(30):
+        p = rng.randrange(len(dt.pairs))
+        i, j = dt.pairs[p]
+        lt, hv = pool[i], pool[j]
+        lc = lt.base_quality_cost + lt.hardness_penalty * h
+        hc = hv.base_quality_cost + hv.hardness_penalty * h
+        a, b = starts[p], starts[p + 1]
+        rows = dict(zip((tp[a:b].astype(np.int64) * K + cp[a:b]).tolist(), range(a, b)))
+        member = list(rows)[rng.randrange(len(rows))]
+        for cell in (member, rng.randrange(K * K)):
+            th, ta = thr[cell // K], thr[cell % K]
+            nb, nr, r_l, r_h, f_c, l_c = og.cell_stats(h, scores[i], lc, hc, lt.latency_s[1],
+                                                       hv.latency_s[1], th, ta)
+            if cell in rows:
+                r = rows[cell]
+                assert (rl[r], rh[r], lat[r]) == (r_l, r_h, l_c)
+                assert math.isclose(fid[r], f_c, rel_tol=1e-9)
+            else:
+                dom = (lat[a:b] <= l_c) & (fid[a:b] <= f_c * (1 + 1e-9))
+                assert dom.any(), (p, cell)
