@@ -381,9 +381,9 @@ __device__ __forceinline__ bool row_task(const Grid& g, const PairConst* __restr
 // minima and compares run on the FP64 pipe, which has the slack -- u64 keys
 // cost four ALU ops per min); bit j of take = the cell passes the row test -- strict
 // prefix-min (F1) or class start within 2 delta of the prefix-min (F3).
-template <bool kFilter, typename F>
+template <bool kFilter, typename F, typename W>
 __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0, int p1, int k,
-                                             F&& visit) {
+                                             F&& visit, W&& window_done) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
   const uint64_t* Sh = slot_hs(g, sm.pc[0].slot);
@@ -481,6 +481,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         const unsigned take = scan(p, sv);
         visit(p, sm.pc[p - p0], w0, sv, take);
       }
+      window_done(w0);                             // staged window still valid here
     }
     __syncwarp();
   }
@@ -526,7 +527,7 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
       const unsigned long long key = order_key_fast(sv[j]);
       if ((take >> j & 1u) && key < cur[j]) atomicMin(bp + bk[j], key);
     }
-  });
+  }, [](int) {});
 }
 
 // ------------------------------------------------- F2: exclusive prefix minima
@@ -805,9 +806,11 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
 
 // F3: candidates = class-start cells within 2 delta (numerator space) of both
 // their row's prefix minimum and their bucket's exclusive prefix minimum.
-// They are appended to an unordered list (one atomic per warp and partner)
-// and counted per (pair, bucket); F5 then groups them by bucket.
-
+// Per window the partners' pass masks go to shared memory; one list
+// reservation per (warp, window) for all partners (the reservation atomic's
+// round trip was the kernel's largest stall), then the candidates are
+// re-evaluated from the staged window (same formulas, bit-identical values),
+// counted per (pair, fine bucket) and appended; F5 groups them by bucket.
 __global__ void __launch_bounds__(kRowWarps * 32, 3)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
@@ -818,12 +821,16 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   int p0, p1, k;
   if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k)) return;
   const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const s_take = smem_raw + sizeof(RowSmem) + warp * (kMaxGroup * 32);
   const uint32_t krep = (uint32_t)g.row_rep[k] * (uint32_t)g.U;
   const bool sorted_thr = *g.sorted != 0;          // first_pos increasing: rep = own rank
   const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
-  const uint32_t* s_nH = sm.nH[threadIdx.x >> 5];
-  row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int w0,
+  const uint32_t* s_nH = sm.nH[warp];
+  const double* s_SHs = sm.SHs[warp];
+  const double* s_LP = sm.LP[warp];
+  int cnt = 0;                                     // this lane's candidates in the window
+  row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
                                            const double* sv, unsigned take) {
     const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
     const double xr = __dmul_rn(dRk, pc.Ll);
@@ -839,32 +846,46 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)
       if (!(sv[j] <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
-    // one list reservation per (window, partner)
-    const int cnt = __popc(take);
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += o;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    s_take[(p - p0) * 32 + lane] = (uint8_t)take;
+    cnt += __popc(take);
+  }, [&](int w0) {
+    const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    cnt = 0;
     if (total == 0) return;
     unsigned long long at0 = 0;
-    if (lane == 31) at0 = atomicAdd(n_list, (unsigned long long)total);
-    int64_t at = (int64_t)__shfl_sync(0xffffffffu, at0, 31) + incl - cnt;
+    if (lane == 0) at0 = atomicAdd(n_list, (unsigned long long)total);
+    int64_t base = (int64_t)__shfl_sync(0xffffffffu, at0, 0);
+    for (int p = p0; p < p1; ++p) {                // partner-major, lane-contiguous runs
+      const unsigned tk = s_take[(p - p0) * 32 + lane];
+      const int c = __popc(tk);
+      int incl = c;
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j) {
-      if (!(take >> j & 1u)) continue;
-      atomicAdd(&bcnt[(int64_t)p * g.nbuckets + bk[j]], 1u);
-      if (at < cap) {
-        // raw numerators; F5 divides (lat = x / n, fid* = S / n)
-        const int t = w0 + lane * kRowT + j;
-        lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
-                         (uint32_t)bk[j], 0u,
-                         __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh)),
-                         sv[j]};
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
       }
-      ++at;
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tot == 0) continue;
+      int64_t at = base + incl - c;
+      base += tot;
+      const PairConst& pc = sm.pc[p - p0];
+      const double xr = __dmul_rn(dRk, pc.Ll);
+#pragma unroll
+      for (int j = 0; j < kRowT; ++j) {
+        if (!(tk >> j & 1u)) continue;
+        const int a = j * kRowPad + lane;
+        const double dnH = u32_to_double(s_nH[a]);
+        const double x = __dadd_rn(xr, __dmul_rn(dnH, pc.Lh));
+        const int b = bucket_of_x(pc, g.nbuckets, x);
+        atomicAdd(&bcnt[(int64_t)p * g.nbuckets + b], 1u);
+        if (at < cap) {
+          // raw numerators; F5 divides (lat = x / n, fid* = S / n)
+          const int t = w0 + lane * kRowT + j;
+          lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
+                           (uint32_t)b, 0u, x, fid_num(pc.bh, pc.ph, dnH, s_SHs[a], s_LP[a])};
+        }
+        ++at;
+      }
     }
   });
 }
@@ -1573,10 +1594,11 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   const dim3 row_grid((unsigned)ceil_div(n_unique, kRowWarps), (unsigned)n_pairs);
   group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups, counters, kMaxGroup);
   const size_t rsm = sizeof(RowSmem);
+  const size_t fsm = rsm + (size_t)kRowWarps * kMaxGroup * 32;   // + per-window pass masks
   HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_min_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
   HADIS_CUDA_TRY(cudaFuncSetAttribute(filter_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
   bucket_min_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cmin);
   auto prefix = [&](const unsigned long long* mins, int nbk, unsigned long long* tm, double* pre) {
     const int tiles = (int)ceil_div(nbk, kPrefTile);
@@ -1586,7 +1608,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   };
   prefix(cmin, nb >> kCoarseShift, ctmin, cpre);
   const DecideOut dout{kept, un, exact_cap, reqbm, req_pair, req_cell, exact_cap, counters};
-  filter_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cpre, bcnt, lst,
+  filter_kernel<<<row_grid, kRowWarps * 32, fsm, st>>>(g, pcs, group_p0, n_groups, cpre, bcnt, lst,
                                                      cand_cap, counters + 5);
   {
     const int64_t tiles = ceil_div(pb, kScanTile);
