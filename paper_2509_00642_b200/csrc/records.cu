@@ -463,11 +463,13 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
     sm.guide_le[i] = rp.guide_le[i];
   }
   for (int i = threadIdx.x; i < U + 2; i += blockDim.x) sm.thr[i] = i < U ? thr[i] : INFINITY;
-  const int64_t tiles = ceil_div(n, kBkTile);
   const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t t0 = tile * kBkTile;
-    const int tn = (int)min((int64_t)kBkTile, n - t0);
+  // one contiguous, even-sized record range per CTA (equal work per SM: 1221
+  // round-robin tiles over 148 CTAs would leave a 9th partial wave at c4)
+  const int64_t chunk = (ceil_div(n, (int64_t)gridDim.x) + 1) & ~(int64_t)1;
+  const int64_t r0 = min(n, (int64_t)blockIdx.x * chunk), r1 = min(n, r0 + chunk);
+  for (int64_t t0 = r0; t0 < r1; t0 += kBkTile) {
+    const int tn = (int)min((int64_t)kBkTile, r1 - t0);
     if (mode == 0 && tn == kBkTile)
       scatter_tile<kVec, true>(h, scores, n, n_light, U, hscale, mode, rp, hfix_rows, bs_rows, sm,
                                t0, tn);
