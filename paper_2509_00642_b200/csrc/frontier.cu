@@ -1356,7 +1356,8 @@ struct Rows {
 };
 
 // bits -> cell list in shared memory -> one row per thread (coalesced stores)
-__global__ void __launch_bounds__(kEmitWords)
+// 6 CTAs/SM: latency bound like decide (-60 us at c4; group_cands the opposite)
+__global__ void __launch_bounds__(kEmitWords, 6)
 emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __restrict__ kept_bm,
                  int64_t words_per_pair, int n_chunks,
                  const unsigned long long* __restrict__ chunk_off, int64_t out_cap, Rows out) {
