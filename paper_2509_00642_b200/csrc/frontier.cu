@@ -926,9 +926,7 @@ constexpr int kDecThreads = 256;
 constexpr int kDecChunk = 1024;
 constexpr int kDecWin = 3072;
 
-// 6 CTAs/SM (<= 42 registers, a few bytes spilled in the rare near-tie path):
-// the pass is load-latency bound, occupancy beats the spill (-80 us at c4)
-__global__ void __launch_bounds__(kDecThreads, 6)
+__global__ void __launch_bounds__(kDecThreads)
 decide_kernel(Grid g, const PairConst* __restrict__ pcs,
               const unsigned long long* __restrict__ counters_ro, int64_t cap,
               const unsigned long long* __restrict__ boff, const uint32_t* __restrict__ bcnt,
