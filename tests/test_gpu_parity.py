@@ -75,18 +75,31 @@ def test_golden_profiles_match_reference(gpu_device, name, exact):
 
 @pytest.mark.parametrize("seed,n,k,hmode", [(1, 1, 5, "u"), (2, 7, 9, "u"), (3, 300, 17, "ties"),
                                             (4, 1000, 40, "u"), (5, 4000, 64, "ties"),
-                                            (6, 2500, 33, "clip"), (7, 129, 128, "u")])
+                                            (6, 2500, 33, "clip"), (7, 129, 128, "u"),
+                                            (8, 50, 1, "u"), (9, 50, 2, "ties"),
+                                            (10, 64, 3, "const"), (11, 200, 6, "grid"),
+                                            (12, 333, 12, "sparse")])
 def test_random_records_match_oracle(gpu_device, seed, n, k, hmode):
+    """Edge cases as the reference's tests have them: one record, one or two
+    thresholds, all-equal hardness, hardness exactly on the thresholds, a
+    non-uniform (guided-binning) grid."""
     rng = np.random.default_rng(seed)
     cat = default_catalog()
     pool = select_candidates(cat, 0.1, 0.1)
     if hmode == "ties":
         h = rng.choice(np.round(rng.uniform(0.0, 1.0, 37), 2), n)
+    elif hmode == "const":
+        h = np.full(n, 0.37)
+    elif hmode == "grid":
+        h = rng.choice(np.linspace(0.0, 1.0, k), n)
     else:
         h = rng.uniform(0.0, 1.0, n)
     sigma = 0.3 if hmode == "clip" else 0.05
     noise = rng.normal(0.0, sigma, n)
-    thr = tuple(rng.permutation(np.linspace(0.0, 1.0, k)).tolist())
+    if hmode == "sparse":
+        thr = tuple(rng.permutation(np.round(np.sort(rng.uniform(0.0, 1.0, k)) ** 3, 6)).tolist())
+    else:
+        thr = tuple(rng.permutation(np.linspace(0.0, 1.0, k)).tolist())
     want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
     got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
     assert tuples(got) == want
