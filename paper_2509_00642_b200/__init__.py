@@ -15,7 +15,8 @@ from .catalog import (Catalog, CatalogError, ModelVariant, default_catalog,  # n
                       make_variant, pareto_prune, scaled_batch_profile, select_candidates)
 from .frontier import (FrontierError, FrontierPoint, FrontierReport,  # noqa: F401
                        frontier_compare, lower_envelope, three_stage_points, two_stage_points)
-from .planner import Plan, PlannerError, fallback_plan, solve, solve_many  # noqa: F401
+from .planner import (Plan, PlannerError, brute_force_solve, fallback_plan, solve,  # noqa: F401
+                      solve_many, validate_plan)
 from .profiler import (THRESHOLD_GRID, CascadeRow, CascadeTable, GridProfiler,  # noqa: F401
                        ProfileError, TableProvenance, load_table, profile_config,
                        profile_records, prompts_hash, save_table)

@@ -5,8 +5,9 @@ Public surface mirrors pkg/src/cascadesim/planner.py:
 ``update_estimate`` (:88), ``solve`` (:217-227), ``fallback_plan``
 (:170-214), the consumers ``PlanCache`` / ``cached_solve`` (:328-367), the
 baselines ``clipper_plan`` / ``proteus_plan`` / ``diffserve_plan``
-(:387-500) and every ``make_planner`` mode (:443-479), plus the batched
-``solve_many`` used by re-plan sweeps.  Every (demand, SLO) point is decided
+(:387-500) and every ``make_planner`` mode (:443-479), the audit helpers
+``brute_force_solve`` / ``validate_plan`` (:230-325, host arithmetic, as in the
+reference), plus the batched ``solve_many`` used by re-plan sweeps.  Every (demand, SLO) point is decided
 on the device by ``hadis_solve_many`` with the reference's exact float64
 expressions and tie-breaks; this module only moves rows/points to the device
 and turns the per-point result back into ``Plan`` objects.
@@ -26,6 +27,7 @@ DEFAULT_QUEUE_ALPHA = 1.5
 EWMA_WEIGHT = 0.3
 SOLVER_DELAY_S = 0.03
 _RATE_FLOOR = 0.01
+_SLACK = 1e-9
 _MAX_POINTS_PER_LAUNCH = 65535
 
 
@@ -271,6 +273,112 @@ def solve(table, catalog, lam: float, queues=None, workers: int = DEFAULT_WORKER
     if lam < 0:
         raise PlannerError("solve: negative demand")
     return solve_many(table, catalog, [lam], queues, workers, t_slo, alpha, label)[0]
+
+
+def _row_models(row) -> list:
+    return [row.light_id] if row.light_id == row.heavy_id else [row.light_id, row.heavy_id]
+
+
+def _row_shares(row) -> dict:
+    out = {row.light_id: row.r_light}
+    out[row.heavy_id] = out.get(row.heavy_id, 0.0) + row.r_heavy
+    return out
+
+
+def _path_latency(row, catalog, batches, lam, queues, alpha) -> float:
+    """sum(latency + drain) over the path's unique models, the reference's
+    left-to-right float order (planner.py:93-104 summed as at :136-140)."""
+    shares = _row_shares(row)
+    total = 0
+    for m in _row_models(row):
+        variant = catalog.by_id(m)
+        total = total + (variant.latency_s[batches[m]]
+                         + queue_delay(queues.get(m, 0.0), lam * shares[m], alpha))
+    return total
+
+
+def brute_force_solve(table, catalog, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
+                      t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA) -> Plan:
+    """Exhaustive cross-check of ``solve`` (planner.py:230-288): every worker
+    split, not only the minimal one, same key (fid, total workers, path, row
+    index).  An audit aid on small instances, computed on the host exactly as
+    the reference does; the overload branch is the device ``fallback_plan``."""
+    rows = list(table.rows if hasattr(table, "rows") else table)
+    if len(rows) > 200 or workers > 16 or len(catalog.batch_sizes) > 5:
+        raise PlannerError("oracle-too-large: brute force capped at "
+                           "200 rows / 16 workers / 5 batch sizes")
+    queues = queues or {}
+    best = None
+    for idx, row in enumerate(rows):
+        shares = _row_shares(row)
+        models = _row_models(row)
+        active = [m for m in models if shares[m] > 0]
+        if not active:
+            continue
+        combos = [()]
+        for _ in active:
+            combos = [c + (b,) for c in combos for b in catalog.batch_sizes]
+        for combo in combos:
+            batches = dict(zip(active, combo))
+            for m in models:
+                batches.setdefault(m, catalog.batch_sizes[0])
+            if len(active) == 1:
+                splits = [{active[0]: a} for a in range(1, workers + 1)]
+            else:
+                splits = [{active[0]: a, active[1]: b} for a in range(1, workers + 1)
+                          for b in range(1, workers + 1 - a)]
+            for xa in splits:
+                if any(xa[m] * catalog.by_id(m).throughput_qps[batches[m]]
+                       < lam * shares[m] - _SLACK for m in active):
+                    continue
+                x = {m: xa.get(m, 0) for m in models}
+                total = sum(x.values())
+                if total > workers:
+                    continue
+                path = _path_latency(row, catalog, batches, lam, queues, alpha)
+                if path > t_slo + _SLACK:
+                    continue
+                key = (row.fidelity_cost, total, path, idx)
+                if best is None or key < best[0]:
+                    best = (key, row, batches, x, path)
+    if best is None:
+        return fallback_plan(list(enumerate(rows)), catalog, lam, queues, workers, t_slo, alpha,
+                             "online")
+    _, row, batches, x, path = best
+    return Plan(row=row, workers=x, batches=batches, lam=lam, queues=dict(queues),
+                fidelity_cost=row.fidelity_cost, path_latency_s=path, infeasible=False,
+                label="online")
+
+
+def validate_plan(plan: Plan, catalog, workers: int = DEFAULT_WORKERS,
+                  t_slo: float = DEFAULT_T_SLO_S, alpha: float = DEFAULT_QUEUE_ALPHA) -> list:
+    """Independent feasibility audit of a plan (planner.py:291-321): the
+    violated constraints as the reference's human-readable strings."""
+    problems = []
+    if plan.total_workers > workers:
+        problems.append(f"worker-budget: {plan.total_workers} > {workers}")
+    shares = _row_shares(plan.row)
+    for m in plan.pair_models():
+        share = shares.get(m, 0.0)
+        x = plan.workers.get(m, 0)
+        batch = plan.batches.get(m)
+        if batch is None:
+            problems.append(f"missing-batch: {m}")
+            continue
+        variant = catalog.by_id(m)
+        if batch not in variant.latency_s:
+            problems.append(f"unprofiled-batch: {m} b={batch}")
+            continue
+        need = plan.lam * share
+        cap = x * variant.throughput_qps[batch]
+        if need > 0 and cap < need - _SLACK:
+            problems.append(f"capacity: {m} x={x} covers {cap:.6f} qps < {need:.6f}")
+        if need > 0 and x < 1:
+            problems.append(f"no-workers: {m} has load but x=0")
+    path = _path_latency(plan.row, catalog, plan.batches, plan.lam, plan.queues, alpha)
+    if path > t_slo + _SLACK:
+        problems.append(f"path-latency: {path:.6f} > {t_slo}")
+    return problems
 
 
 def fallback_plan(indexed_rows, catalog, lam, queues, workers, t_slo, alpha, label):

@@ -590,3 +590,18 @@ def test_full_scale_properties(gpu_device, name):
             else:
                 dom = (lat[a:b] <= l_c) & (fid[a:b] <= f_c * (1 + 1e-9))
                 assert dom.any(), (p, cell)
+
+
+def test_brute_force_solve_matches_reference(gpu_device):
+    """brute_force_solve on every golden instance, the overload fallback included."""
+    from paper_2509_00642_b200.planner import brute_force_solve
+    for case in load_json("planner_random200")["cases"]:
+        cat = catalog_from_doc(case["catalog"])
+        rows = rows_ns(case["rows"])
+        try:
+            plan = brute_force_solve(rows, cat, case["lam"], case["queues"], case["workers"],
+                                     case["t_slo"], case["alpha"])
+        except PlannerError as exc:
+            assert case["brute"] is None and case["brute_error"] == str(exc)
+            continue
+        _plan_matches(plan, case["brute"], rows)
