@@ -11,8 +11,9 @@ reference's Python interface for that path.
 
 __version__ = "0.1.0"
 
-from .catalog import (Catalog, CatalogError, ModelVariant, default_catalog,  # noqa: F401
-                      make_variant, pareto_prune, scaled_batch_profile, select_candidates)
+from .catalog import (Catalog, CatalogError, ModelVariant, batch_latency,  # noqa: F401
+                      default_catalog, load_catalog, make_variant, pareto_prune,
+                      scaled_batch_profile, select_candidates)
 from .frontier import (FrontierError, FrontierPoint, FrontierReport,  # noqa: F401
                        frontier_compare, lower_envelope, three_stage_points, two_stage_points)
 from .planner import (Plan, PlannerError, brute_force_solve, fallback_plan, solve,  # noqa: F401

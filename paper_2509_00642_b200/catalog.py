@@ -112,6 +112,58 @@ def make_variant(variant_id, latency_s, base_quality_cost, hardness_penalty, acc
                         accept_params=accept_params)
 
 
+def batch_latency(variant, batch: int) -> float:
+    """Exact latency lookup; an unprofiled batch size is an error (catalog.py:163-168)."""
+    try:
+        return variant.latency_s[batch]
+    except KeyError:
+        raise CatalogError(f"batch-not-profiled: {variant.id} b={batch}") from None
+
+
+def load_catalog(path: str) -> Catalog:
+    """Catalog from the reference's YAML file format (catalog.py:289-331): same
+    keys (batch_sizes, batch_scaling_beta, calibrated, variants[] with id,
+    base_quality_cost, hardness_penalty, accept_params and latency_s table or
+    latency_b1) and the same first-violation messages."""
+    import yaml
+    with open(path, "r", encoding="utf-8") as fh:
+        raw = yaml.safe_load(fh)
+    if not isinstance(raw, dict):
+        raise CatalogError("catalog file: top level must be a mapping")
+    batch_sizes = tuple(raw.get("batch_sizes", DEFAULT_BATCH_SIZES))
+    beta = float(raw.get("batch_scaling_beta", DEFAULT_BATCH_BETA))
+    entries = raw.get("variants")
+    if not isinstance(entries, list) or not entries:
+        raise CatalogError("variants: must be a non-empty list")
+    variants = []
+    for i, entry in enumerate(entries):
+        where = f"variants[{i}]"
+        if not isinstance(entry, dict):
+            raise CatalogError(f"{where}: must be a mapping")
+        try:
+            fields = (entry["id"], float(entry["base_quality_cost"]),
+                      float(entry["hardness_penalty"]),
+                      tuple(float(x) for x in entry["accept_params"]))
+        except KeyError as exc:
+            raise CatalogError(f"{where}.{exc.args[0]}: missing") from None
+        vid, cost, penalty, accept = fields
+        if len(accept) != 2:
+            raise CatalogError(f"{where}.accept_params: expected [a, s]")
+        lat = entry.get("latency_s")
+        if isinstance(lat, dict):
+            latency = {int(b): float(x) for b, x in lat.items()}
+            missing = [b for b in batch_sizes if b not in latency]
+            if tuple(sorted(latency)) != batch_sizes and missing:
+                raise CatalogError(f"{where}.latency_s: missing batch sizes {missing}")
+        elif "latency_b1" in entry:
+            latency = scaled_batch_profile(float(entry["latency_b1"]), batch_sizes, beta)
+        else:
+            raise CatalogError(f"{where}.latency_s: give a table or latency_b1")
+        variants.append(make_variant(vid, latency, cost, penalty, (accept[0], accept[1])))
+    return Catalog(variants=tuple(variants), batch_sizes=batch_sizes,
+                   calibrated=bool(raw.get("calibrated", False)))
+
+
 def check_catalog(cat) -> None:
     """Validation rules and messages of catalog.py:122-160."""
     if not cat.variants:
