@@ -287,6 +287,7 @@ class GridProfiler:
             raise ValueError("layout must be 'bucketed' or 'original'")
         self.layout = layout
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._stats_pin = None
         self._store = None
 
     def _bucket_store(self, n_light):
@@ -412,7 +413,7 @@ class GridProfiler:
                    r_heavy=torch.empty(out_cap, dtype=torch.float64, device=dev),
                    fid=torch.empty(out_cap, dtype=torch.float64, device=dev),
                    lat=torch.empty(out_cap, dtype=torch.float64, device=dev))
-        stats = torch.zeros(_lib.ST_PAIR0 + P, dtype=torch.int64, device=dev)
+        stats = torch.zeros(_lib.ST_PAIR0 + P + 1, dtype=torch.int64, device=dev)  # + bad flag
         p = _lib.ptr
         _lib.check(self.lib.hadis_pair_frontiers(
             p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(plan.d_slot),
@@ -421,14 +422,27 @@ class GridProfiler:
             cand_cap, exact_cap, out_cap, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]),
             p(out["r_light"]), p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
             _lib.stream_handle(state["stream"])), "hadis_pair_frontiers")
+        # the record-validation flag rides along, so finish() needs one device read
+        if state["stream"] is None:
+            stats[-1:].copy_(self.bad)
+        else:
+            with torch.cuda.stream(state["stream"]):
+                stats[-1:].copy_(self.bad)
         state.update(out=out, stats=stats, caps=caps)
 
     def finish(self, state) -> DeviceTable:
         """Synchronise, check device-side status, grow capacities and rerun if needed."""
         plan = state["plan"]
         for _ in range(6):
-            stats = state["stats"].cpu().tolist()
-            if int(self.bad.item()):
+            dev_stats = state["stats"]
+            pin = self._stats_pin
+            if pin is None or pin.numel() < dev_stats.numel():
+                pin = self._stats_pin = self.torch.empty(dev_stats.numel(),
+                                                         dtype=self.torch.int64).pin_memory()
+            pin[:dev_stats.numel()].copy_(dev_stats, non_blocking=True)
+            (state["stream"] or self.torch.cuda.current_stream()).synchronize()
+            stats = pin[:dev_stats.numel()].tolist()
+            if stats[-1]:
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW] == 0:
                 break
