@@ -336,8 +336,9 @@ struct Cands {
 // non-decreasing in t (the reject count is), so a cell whose S exceeds the
 // exclusive prefix-min of S over the earlier cells of its row is dominated by
 // one of them (lat <=, fid* <).  The row is walked in windows of kRowWin
-// cells: the warp stages the window's statistics as doubles in shared memory
-// (shared by every heavy partner of the slot); per partner, lane l evaluates
+// cells: the warp stages the window's statistics in shared memory (nH as u32,
+// the hardness terms as doubles; shared by every heavy partner of the slot);
+// per partner, lane l evaluates
 // its kRowT contiguous cells, one warp scan of the lane minima gives each
 // lane its carry-in, and the per-cell test is one compare.  The [j][33]
 // layout keeps staging stores and per-lane reads conflict-free.  Rows that
