@@ -344,7 +344,10 @@ struct Cands {
 // layout keeps staging stores and per-lane reads conflict-free.  Rows that
 // repeat an earlier row's R[k] (same row class) are exact duplicates and are
 // skipped.
-constexpr int kRowWarps = 8;
+#ifndef HADIS_ROW_WARPS
+#define HADIS_ROW_WARPS 8
+#endif
+constexpr int kRowWarps = HADIS_ROW_WARPS;
 constexpr int kCoarseShift = 4;      // F1/F3 latency buckets: the fine ones >> 4
                                      // (3 and 5 measured: F1 vs candidate trade-off, no gain)
 constexpr int kMaxGroup = 64;        // heavy partners per light slot (pool <= 65 models)
@@ -493,7 +496,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 // dominated by an earlier cell of its row, which sits in the same or a lower
 // bucket).  Reads the current minima first (all in flight): most cells do
 // not lower them.
-__global__ void __launch_bounds__(kRowWarps * 32, 4)
+__global__ void __launch_bounds__(kRowWarps * 32, 32 / kRowWarps)
 bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
                   const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -812,7 +815,7 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
 // round trip was the kernel's largest stall), then the candidates are
 // re-evaluated from the staged window (same formulas, bit-identical values),
 // counted per (pair, fine bucket) and appended; F5 groups them by bucket.
-__global__ void __launch_bounds__(kRowWarps * 32, 3)
+__global__ void __launch_bounds__(kRowWarps * 32, 24 / kRowWarps)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
               uint32_t* __restrict__ bcnt, Cands lst, int64_t cap,
@@ -1619,11 +1622,12 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
     tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
-  group_cands_kernel<<<kNumSMs * 8, 256, 0, st>>>(lst, counters + 5, cand_cap, nb, (double)n, boff,
+  // grid sizes of the two grid-stride passes measured at c4 (4 / 32 CTAs per SM)
+  group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(lst, counters + 5, cand_cap, nb, (double)n, boff,
                                                   bcur, grp, bmin);
   prefix(bmin, nb, tmin, gpre);                    // exact fine G for decide
   HADIS_LAUNCH_CHECK();
-  decide_kernel<<<kNumSMs * 8, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
+  decide_kernel<<<kNumSMs * 32, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
   if (row_smem > 48 * 1024)
