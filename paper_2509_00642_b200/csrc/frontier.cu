@@ -159,8 +159,9 @@ __device__ __forceinline__ void numerators_of(const Grid& g, const PairConst& pc
 
 // bucket of a latency numerator; monotone non-decreasing in x (hence in lat)
 __device__ __forceinline__ int bucket_of_x(const PairConst& pc, int nbuckets, double x) {
-  // floor + saturating convert in one instruction (NaN -> INT_MIN -> bucket 0)
-  const int b = __double2int_rd(__fma_rn(x, pc.scale_x, pc.off_x));
+  // floor without the XU convert: adding 1.5 * 2^52 rounding down leaves
+  // floor(y) in the low mantissa word (|y| < 2^51; y < 0 gives -1 -> bucket 0)
+  const int b = __double2loint(__dadd_rd(__fma_rn(x, pc.scale_x, pc.off_x), 6755399441055744.0));
   return min(max(b, 0), nbuckets - 1);
 }
 
