@@ -212,7 +212,8 @@ def run_ours(args, cfg):
 
     from paper_2509_00642_b200 import _lib, synth
     from paper_2509_00642_b200.profiler import GridProfiler, pair_list
-    from paper_2509_00642_b200.sharding import FIELDS, gather_rows, shard_pairs
+    from paper_2509_00642_b200.sharding import (FIELDS, gather_rows, shard_light_groups,
+                                                shard_pairs)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -229,18 +230,24 @@ def run_ours(args, cfg):
 
     pool, h, noise, scores = synth.records(cfg)
     pairs = pair_list(pool)
-    offset, mine = shard_pairs(pairs, world, rank)
     thr = cfg.thresholds
     n = cfg.n_queries
-    # pinned host copies for the e2e leg; resident device copies for `value`
-    slots = sorted({i for i, _ in mine}) if mine else [0]
-    s0, s1 = slots[0], slots[-1] + 1
     h_pin = torch.from_numpy(h).pin_memory()
-    sc_pin = torch.from_numpy(np.ascontiguousarray(scores[s0:s1])).pin_memory()
     d_h = h_pin.to(dev)
-    d_sc = torch.zeros((len(pool) - 1, n), dtype=torch.float64, device=dev)
-    d_sc[s0:s1] = sc_pin.to(dev)
-    prof = GridProfiler(pool, d_h, d_sc, device=dev)
+    # pinned host copies for the e2e leg; resident device copies for `value`
+    if world > 1:
+        # whole light-model groups per rank; the rank holds only its light
+        # models' score rows (compact, slot-mapped)
+        offset, mine = shard_light_groups(pairs, world, rank)
+        slots = sorted({i for i, _ in mine}) if mine else [0]
+        sc_pin = torch.from_numpy(np.ascontiguousarray(scores[slots])).pin_memory()
+        d_sc = sc_pin.to(dev)
+        prof = GridProfiler(pool, d_h, d_sc, device=dev, slots=slots)
+    else:
+        offset, mine = shard_pairs(pairs, world, rank)
+        sc_pin = torch.from_numpy(np.ascontiguousarray(scores)).pin_memory()
+        d_sc = sc_pin.to(dev)
+        prof = GridProfiler(pool, d_h, d_sc, device=dev)
     plan = prof.plan(thr, pairs=mine) if mine else None
     stream = torch.cuda.current_stream()
 
@@ -326,7 +333,7 @@ def run_ours(args, cfg):
             t0 = time.perf_counter()
             if plan is not None:
                 d_h.copy_(h_pin, non_blocking=True)
-                d_sc[s0:s1].copy_(sc_pin, non_blocking=True)
+                d_sc.copy_(sc_pin, non_blocking=True)
             arrays = step()
             d2h = 0
             for f, v in arrays.items():           # D2H into pinned host buffers

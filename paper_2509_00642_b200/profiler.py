@@ -239,15 +239,15 @@ class ProfilePlan:
         self.pairs = pair_list(prof.pool) if pairs is None else list(pairs)
         if not self.pairs:
             raise ProfileError("profile_records: no pairs to profile")
-        slots = sorted({i for i, _ in self.pairs})
-        self.slot0 = slots[0]
-        self.n_light = slots[-1] - slots[0] + 1
+        rows = sorted({prof.row_of(i) for i, _ in self.pairs})     # score rows used
+        self.slot0 = rows[0]
+        self.n_light = rows[-1] - rows[0] + 1
         self.U = len(self.grid.unique)
         self.P = len(self.pairs)
         self.d_u = torch.tensor(self.grid.unique, dtype=torch.float64, device=dev)
         self.d_first = torch.tensor(self.grid.first_pos, dtype=torch.int32, device=dev)
-        self.d_slot = torch.tensor([i - self.slot0 for i, _ in self.pairs], dtype=torch.int32,
-                                   device=dev)
+        self.d_slot = torch.tensor([prof.row_of(i) - self.slot0 for i, _ in self.pairs],
+                                   dtype=torch.int32, device=dev)
         self.d_params = torch.from_numpy(pair_params(prof.pool, self.pairs)).to(dev)
         cells = self.U * self.U * self.P
         cand = int(min(cells, max(1 << 20, cells // 8)))
@@ -264,7 +264,7 @@ class GridProfiler:
     ``run`` profiles one threshold grid; ``launch``/``finish`` split it into an
     asynchronous enqueue and a synchronising check for pipelined callers."""
 
-    def __init__(self, pool, h, scores, device=None, layout="bucketed"):
+    def __init__(self, pool, h, scores, device=None, layout="bucketed", slots=None):
         torch = _lib.torch_cuda()
         self.torch = torch
         self.pool = list(pool)
@@ -276,9 +276,14 @@ class GridProfiler:
         self.n = int(self.h.shape[0])
         if self.n == 0:
             raise ProfileError("profile_config: empty prompt population")
+        # slots: pool light index of each score row when scores hold a subset
+        # of the light models (a multi-GPU shard); default row i = pool model i
+        self.slots = None if slots is None else [int(x) for x in slots]
+        want_rows = len(self.pool) - 1 if self.slots is None else len(self.slots)
         if self.scores.dim() != 2 or self.scores.shape[1] != self.n or \
-                self.scores.shape[0] < len(self.pool) - 1:
+                self.scores.shape[0] < want_rows:
             raise ProfileError("profile_records: scores must be [n_models - 1, n_records]")
+        self._row_of = None if self.slots is None else {m: r for r, m in enumerate(self.slots)}
         self.lib = _lib.load()
         self.shift = self.lib.hadis_hfix_shift(self.n)
         self._ws = None
@@ -289,6 +294,16 @@ class GridProfiler:
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._stats_pin = None
         self._store = None
+
+    def row_of(self, light_index: int) -> int:
+        """Score row holding pool model ``light_index`` as the light stage."""
+        if self._row_of is None:
+            return light_index
+        try:
+            return self._row_of[light_index]
+        except KeyError:
+            raise ProfileError(f"profile_records: no score row for light model {light_index}") \
+                from None
 
     def _bucket_store(self, n_light):
         """Row-bucketed record store buffers (hfix u64[n], bs u16 model quads, row plan)."""

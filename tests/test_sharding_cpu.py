@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2509_00642_b200.sharding import FIELDS, gather_rows, shard_pairs
+from paper_2509_00642_b200.sharding import FIELDS, gather_rows, shard_light_groups, shard_pairs
 
 
 def _free_port():
@@ -32,6 +32,25 @@ def test_shard_pairs_partition(n, world):
     assert max(sizes) - min(sizes) <= 1
 
 
+@pytest.mark.parametrize("models,world", [(16, 8), (16, 2), (16, 3), (8, 8), (4, 8), (16, 16),
+                                          (2, 1)])
+def test_shard_light_groups_partition(models, world):
+    pairs = [(i, j) for i in range(models) for j in range(i + 1, models)]
+    seen = []
+    loads = []
+    for r in range(world):
+        ids, mine = shard_light_groups(pairs, world, r)
+        assert ids == sorted(ids) and mine == [pairs[i] for i in ids]
+        seen.extend(ids)
+        loads.append(len(ids))
+    assert sorted(seen) == list(range(len(pairs)))
+    share = -(-len(pairs) // world)
+    assert max(loads) <= share + 1
+    if (models, world) == (16, 8):              # c4 on 8 GPUs: {15}, {14, 1}, {13, 2}, ...
+        lights = [len({p[0] for p in shard_light_groups(pairs, 8, r)[1]}) for r in range(8)]
+        assert loads == [15] * 8 and max(lights) == 2
+
+
 def _rows_for(pair_ids):
     # deterministic fake per-pair rows: pair p has p % 3 + 1 rows
     rows = {f: [] for f in FIELDS}
@@ -47,17 +66,26 @@ def _rows_for(pair_ids):
     return rows
 
 
-def _worker(rank, world, port, n_pairs, out_path):
+def _worker(rank, world, port, n_pairs, out_path, by_light=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    pairs = list(range(n_pairs))
-    off, mine = shard_pairs(pairs, world, rank)
+    if by_light:                                 # pairs of a 5-model pool, light-group shards
+        plist = [(i, j) for i in range(5) for j in range(i + 1, 5)][:n_pairs]
+        off, mine_pairs = shard_light_groups(plist, world, rank)
+        mine = list(off)
+        local_ids = list(range(len(mine)))
+    else:
+        pairs = list(range(n_pairs))
+        off, mine = shard_pairs(pairs, world, rank)
+        local_ids = None
     rows = _rows_for(mine)
+    if local_ids is not None:                    # rows carry local pair ids 0..len(mine)-1
+        rows["pair"] = [mine.index(p) for p in rows["pair"]]
     arrays = {}
     for f in FIELDS:
         if f in ("pair", "theta_pos", "tau_pos"):
             t = torch.tensor(rows[f], dtype=torch.int32)
-            arrays[f] = t - off if f == "pair" else t     # local pair ids
+            arrays[f] = t - off if (f == "pair" and not by_light) else t   # local pair ids
         else:
             arrays[f] = torch.tensor(rows[f], dtype=torch.float64)
     merged = gather_rows(torch, dist, arrays, off, torch.device("cpu"))
@@ -66,10 +94,11 @@ def _worker(rank, world, port, n_pairs, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_pairs", [6, 7, 1])
-def test_gather_rows_gloo_world2(tmp_path, n_pairs):
+@pytest.mark.parametrize("n_pairs,by_light", [(6, False), (7, False), (1, False), (10, True),
+                                              (7, True)])
+def test_gather_rows_gloo_world2(tmp_path, n_pairs, by_light):
     out = str(tmp_path / "merged.pt")
-    mp.spawn(_worker, args=(2, _free_port(), n_pairs, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), n_pairs, out, by_light), nprocs=2, join=True)
     merged = torch.load(out)
     want = _rows_for(range(n_pairs))
     for f in FIELDS:
