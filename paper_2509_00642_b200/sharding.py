@@ -125,3 +125,35 @@ def profile_sharded(prof, thresholds, dist, exact_fid=False, group=None):
         arrays = {f: (empty_i if f in ("pair", "theta_pos", "tau_pos") else empty_d)
                   for f in FIELDS}
     return pairs, gather_rows(torch, dist, arrays, ids, prof.device, group)
+
+
+def solve_sharded(table, catalog, lams, queues=None, workers=16, t_slo=60.0, alpha=1.5,
+                  dist=None, group=None, label="online"):
+    """Allocation search over many (demand, SLO) points on every rank (SURVEY
+    §8(e), c5): contiguous point chunks per rank (points are independent),
+    ``planner.solve_many`` on each rank's GPU, then one all-gather of the
+    plans; the list is in input order on every rank."""
+    import numpy as np
+
+    from .planner import solve_many
+    lams = [float(x) for x in lams]
+    n = len(lams)
+
+    def per_point(v, cast):
+        if v is None or np.isscalar(v) or isinstance(v, dict):
+            return [v] * n
+        v = list(v)
+        return [cast(x) for x in v] if cast else v
+
+    qs = per_point(queues, None)
+    ws = per_point(workers, int)
+    ts = per_point(t_slo, float)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    stop = start + base + (1 if rank < extra else 0)
+    mine = (solve_many(table, catalog, lams[start:stop], qs[start:stop], ws[start:stop],
+                       ts[start:stop], alpha, label) if stop > start else [])
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    return [p for part in parts for p in part]

@@ -12,7 +12,7 @@ import torch.distributed as dist  # noqa: E402
 
 from paper_2509_00642_b200 import synth  # noqa: E402
 from paper_2509_00642_b200.profiler import GridProfiler, light_scores  # noqa: E402
-from paper_2509_00642_b200.sharding import FIELDS, profile_sharded  # noqa: E402
+from paper_2509_00642_b200.sharding import FIELDS, profile_sharded, solve_sharded  # noqa: E402
 
 
 def main():
@@ -30,8 +30,22 @@ def main():
             a = merged[f].cpu().numpy()
             b = getattr(single, f).cpu().numpy().astype(a.dtype)
             assert np.array_equal(a, b), f
+    # c5-style allocation search sharded over the points
+    from paper_2509_00642_b200.planner import solve_many
+    from paper_2509_00642_b200.profiler import rows_from_device
+    table_rows = rows_from_device(prof.run(cfg.thresholds), pool, cfg.thresholds)
+    cat = cfg.catalog()
+    lams = [0.1 * (i + 1) for i in range(97)] + [0.0, 500.0]
+    slos = [(15.0, 30.0, 60.0, 90.0)[i % 4] for i in range(len(lams))]
+    plans = solve_sharded(table_rows, cat, lams, None, 8, slos, 1.5, dist=dist)
+    if dist.get_rank() == 0:
+        want = solve_many(table_rows, cat, lams, None, 8, slos, 1.5)
+        assert len(plans) == len(want)
+        for a, b in zip(plans, want):
+            assert (a.row, a.workers, a.batches, a.path_latency_s, a.infeasible) == \
+                (b.row, b.workers, b.batches, b.path_latency_s, b.infeasible)
         print(f"sharded OK: world={dist.get_world_size()} rows={len(merged['pair'])} "
-              f"pairs={len(pairs)}", flush=True)
+              f"pairs={len(pairs)} plans={len(plans)}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
