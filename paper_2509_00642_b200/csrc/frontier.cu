@@ -332,6 +332,13 @@ struct Cands {
   Cand* c;
 };
 
+// F3's unordered candidate list: 16 bytes (x and the bucket are recomputed
+// from the cell in F5, bit-identically: same prefix-table counts, same ops)
+struct __align__(16) ListCand {
+  uint32_t pair, cell;   // cell = k * U + t (representative)
+  double S;              // fid* numerator
+};
+
 // Row passes F1 / F3.  One warp per (light slot, theta rank k); a CTA holds
 // kRowWarps rows of one slot group.  Along a row the latency numerator x is
 // non-decreasing in t (the reject count is), so a cell whose S exceeds the
@@ -819,7 +826,7 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
 __global__ void __launch_bounds__(kRowWarps * 32, 24 / kRowWarps)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
-              uint32_t* __restrict__ bcnt, Cands lst, int64_t cap,
+              uint32_t* __restrict__ bcnt, ListCand* __restrict__ lst, int64_t cap,
               unsigned long long* __restrict__ n_list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
@@ -886,8 +893,9 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
         if (at < cap) {
           // raw numerators; F5 divides (lat = x / n, fid* = S / n)
           const int t = w0 + lane * kRowT + j;
-          lst.c[at] = Cand{(uint32_t)p, krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
-                           (uint32_t)b, 0u, x, fid_num(pc.bh, pc.ph, dnH, s_SHs[a], s_LP[a])};
+          lst[at] = ListCand{(uint32_t)p,
+                             krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
+                             fid_num(pc.bh, pc.ph, dnH, s_SHs[a], s_LP[a])};
         }
         ++at;
       }
@@ -896,7 +904,9 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
 }
 
 // F5: group the candidate list by (pair, bucket) with the scanned counts
-__global__ void group_cands_kernel(Cands lst, const unsigned long long* __restrict__ n_list,
+__global__ void group_cands_kernel(Grid g, const PairConst* __restrict__ pcs,
+                                   const ListCand* __restrict__ lst,
+                                   const unsigned long long* __restrict__ n_list,
                                    int64_t cap, int nbuckets, double dn,
                                    const unsigned long long* __restrict__ boff,
                                    uint32_t* __restrict__ bcur, Cands grp,
@@ -904,8 +914,17 @@ __global__ void group_cands_kernel(Cands lst, const unsigned long long* __restri
   if ((int64_t)*n_list > cap) return;
   const int64_t m = (int64_t)*n_list;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t n = (uint32_t)g.n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    Cand cd = lst.c[i];
+    const ListCand lc = lst[i];
+    const PairConst& pc = pcs[lc.pair];
+    // x exactly as F3 formed it: the representative cell has the same (R_k, nr)
+    const uint32_t* C = slot_cnt(g, pc.slot);
+    const uint32_t k = lc.cell / (uint32_t)g.U, t = lc.cell - k * (uint32_t)g.U;
+    const uint32_t Rk = C[(int64_t)k * g.B1 + g.U];
+    const uint32_t nH = (n - Rk) + C[(int64_t)k * g.B1 + t];
+    const double x = __dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh));
+    Cand cd{lc.pair, lc.cell, (uint32_t)bucket_of_x(pc, nbuckets, x), 0u, x, lc.S};
     const int64_t key = (int64_t)cd.pair * nbuckets + cd.bucket;
     // fine-bucket minima over the candidates: every cell F1/F3 pruned is
     // beaten by a candidate at lower-or-equal latency, so the exclusive
@@ -1476,7 +1495,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.bcur = take(4 * pb);
   L.boff = take(8 * (pb + 1));
   L.grp = take(sizeof(Cand) * cap);
-  L.lst = take(sizeof(Cand) * cap);
+  L.lst = take(sizeof(ListCand) * cap);
   L.kept = take(4 * words);
   L.reqbm = take(4 * words);
   L.un[0] = take(4 * ecap); L.un[1] = take(4 * ecap); L.un[2] = take(4 * ecap);
@@ -1557,7 +1576,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   uint32_t* bcur = (uint32_t*)P(L.bcur);
   unsigned long long* boff = (unsigned long long*)P(L.boff);
   Cands grp{(Cand*)P(L.grp)};
-  Cands lst{(Cand*)P(L.lst)};
+  ListCand* lst = (ListCand*)P(L.lst);
   uint32_t* kept = (uint32_t*)P(L.kept);
   uint32_t* reqbm = (uint32_t*)P(L.reqbm);
   Uncertain un{(uint32_t*)P(L.un[0]), (uint32_t*)P(L.un[1]), (uint32_t*)P(L.un[2])};
@@ -1624,7 +1643,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
   // grid sizes of the two grid-stride passes measured at c4 (4 / 32 CTAs per SM)
-  group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(lst, counters + 5, cand_cap, nb, (double)n, boff,
+  group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, lst, counters + 5, cand_cap, nb, (double)n, boff,
                                                   bcur, grp, bmin);
   prefix(bmin, nb, tmin, gpre);                    // exact fine G for decide
   HADIS_LAUNCH_CHECK();
