@@ -967,7 +967,7 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     const int p = (int)cd.pair;
     const int64_t key = (int64_t)p * g.nbuckets + cd.bucket;
     const int64_t s0 = (int64_t)boff[key];
-    const int64_t s1 = min(s0 + (int64_t)bcnt[key], m);
+    const int64_t s1 = min((int64_t)boff[key + 1], m);   // exclusive scan: next start
     const double GS = gpre[key];
     const double d2 = pcs[p].delta2;
     const double G = __ddiv_rn(GS, dn);
