@@ -352,14 +352,11 @@ struct __align__(16) ListCand {
 // layout keeps staging stores and per-lane reads conflict-free.  Rows that
 // repeat an earlier row's R[k] (same row class) are exact duplicates and are
 // skipped.
-#ifndef HADIS_ROW_WARPS
-#define HADIS_ROW_WARPS 8
-#endif
-constexpr int kRowWarps = HADIS_ROW_WARPS;
+constexpr int kRowWarps = 8;         // rows per CTA (4: no gain)
 constexpr int kCoarseShift = 4;      // F1/F3 latency buckets: the fine ones >> 4
                                      // (3 and 5 measured: F1 vs candidate trade-off, no gain)
 constexpr int kMaxGroup = 64;        // heavy partners per light slot (pool <= 65 models)
-constexpr int kRowT = 8;             // cells per lane per window
+constexpr int kRowT = 4;             // cells per lane per window (8: F3 +40 us; 2: slower)
 constexpr int kRowWin = 32 * kRowT;  // cells per window
 constexpr int kRowPad = 33;
 
@@ -504,7 +501,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 // dominated by an earlier cell of its row, which sits in the same or a lower
 // bucket).  Reads the current minima first (all in flight): most cells do
 // not lower them.
-__global__ void __launch_bounds__(kRowWarps * 32, 32 / kRowWarps)
+__global__ void __launch_bounds__(kRowWarps * 32, 32 / kRowWarps)   // 4 CTAs/SM at 8 warps
 bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
                   const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -823,7 +820,7 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
 // round trip was the kernel's largest stall), then the candidates are
 // re-evaluated from the staged window (same formulas, bit-identical values),
 // counted per (pair, fine bucket) and appended; F5 groups them by bucket.
-__global__ void __launch_bounds__(kRowWarps * 32, 24 / kRowWarps)
+__global__ void __launch_bounds__(kRowWarps * 32, 32 / kRowWarps)   // 4 CTAs/SM (3, 5, 6: slower)
 filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
               const int32_t* __restrict__ n_groups, const double* __restrict__ gpre,
               uint32_t* __restrict__ bcnt, ListCand* __restrict__ lst, int64_t cap,
