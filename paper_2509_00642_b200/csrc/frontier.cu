@@ -1321,7 +1321,7 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
 // The kept bitmap is cut into chunks of kEmitWords words (per pair); chunk
 // popcounts -> device-wide scan -> one CTA per chunk writes its rows, so rows
 // come out pair-major and, within a pair, in (theta rank, tau rank) order.
-constexpr int kEmitWords = 256;   // = emit CTA size
+constexpr int kEmitWords = 256;   // = emit CTA size (64 / 128 / 512 measured: no gain)
 
 __global__ void __launch_bounds__(kScanThreads)
 count_chunks_kernel(const uint32_t* __restrict__ kept_bm, int64_t words_per_pair, int n_chunks,
@@ -1503,7 +1503,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.pwplan = take(sizeof(PwPlan));
   const int64_t pw_batch = std::min<int64_t>(std::max(ecap, out_cap), kPwCellsPerLaunch);
   L.pwvals = take(8 * (int64_t)kPwPlanNodes * pw_batch);
-  const int64_t n_cw = ceil_div((cells + 31) / 32, 256) * n_pairs;    // emit chunks
+  const int64_t n_cw = ceil_div((cells + 31) / 32, kEmitWords) * n_pairs;   // emit chunks
   L.pair_rows = take(4 * n_cw);
   L.chunk_off = take(8 * (n_cw + 1));
   L.ctsum = take(8 * (ceil_div(n_cw, 4096) + 1));
