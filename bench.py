@@ -307,15 +307,16 @@ def run_ours(args, cfg):
                                            stage(4, 5))
 
     # ---- e2e: host buffers, H2D + build + D2H of the row arrays every step.
-    # One rank: TablePipeline (double-buffered; set i's H2D overlaps set i-1's
-    # build and set i-2's D2H).  Several ranks: sequential steps, each rank its shard.
+    # TablePipeline on every rank (double-buffered; set i's H2D overlaps set
+    # i-1's build and set i-2's D2H); with N ranks each streams its own shard.
     h2d = (h_pin.numel() + sc_pin.numel()) * 8 if plan is not None else 0
     d2h = 0
     barrier()
     e2e_steps = max(3, min(args.steps, 8))
-    if world == 1 and plan is not None:
+    if plan is not None:
         from paper_2509_00642_b200.profiler import TablePipeline
-        pipe = TablePipeline(pool, n, len(pool) - 1, thr, pairs=mine, device=dev)
+        pipe = TablePipeline(pool, n, sc_pin.shape[0], thr, pairs=mine, device=dev,
+                             score_slots=slots if world > 1 else None)
         pipe.warm(h_pin, sc_pin)
         pipe.run([(h_pin, sc_pin)] * 2)                         # warm the streams
         torch.cuda.synchronize()
@@ -324,8 +325,9 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         e2e_ms = [(time.perf_counter() - t0) * 1e3 / e2e_steps]
         d2h = res[-1][2]
-        if res[-1][1] != rows:
-            raise RuntimeError(f"e2e pipeline produced {res[-1][1]} rows, expected {rows}")
+        if res[-1][1] != int(last["pair"].shape[0]):
+            raise RuntimeError(f"e2e pipeline produced {res[-1][1]} rows, expected "
+                               f"{int(last['pair'].shape[0])}")
     else:
         e2e_ms = []
         out_pin = {}

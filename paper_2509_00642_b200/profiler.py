@@ -497,7 +497,10 @@ class TablePipeline:
 
     FIELDS = ("pair", "theta_pos", "tau_pos", "r_light", "r_heavy", "fid", "lat")
 
-    def __init__(self, pool, n, n_rows_scores, thresholds, pairs=None, device=None):
+    def __init__(self, pool, n, n_rows_scores, thresholds, pairs=None, device=None,
+                 score_slots=None):
+        """score_slots: pool light index of each score row when the record sets
+        carry only some light models' scores (a multi-GPU shard)."""
         torch = _lib.torch_cuda()
         self.torch = torch
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -505,7 +508,7 @@ class TablePipeline:
         for _ in range(2):
             d_h = torch.zeros(n, dtype=torch.float64, device=self.device)
             d_sc = torch.zeros((n_rows_scores, n), dtype=torch.float64, device=self.device)
-            prof = GridProfiler(pool, d_h, d_sc, device=self.device)
+            prof = GridProfiler(pool, d_h, d_sc, device=self.device, slots=score_slots)
             self.slots.append(dict(h=d_h, sc=d_sc, prof=prof, plan=prof.plan(thresholds, pairs),
                                    replay=None, ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(),
                                    ev_out=torch.cuda.Event(), busy=False))
