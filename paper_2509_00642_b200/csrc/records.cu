@@ -199,7 +199,15 @@ bucket_count_kernel(const double* __restrict__ h, int64_t n, const double* __res
     atomicAdd(&s_cnt[plan_bin<false>(mode, s_thr, U, s_guide, x)], 1u);
   };
   if (vec) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {    // four 16-byte loads in flight
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = h2[i + u * stride];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { one(v[u].x); one(v[u].y); }
+    }
+    for (; i < n2; i += stride) {
       const double2 v = h2[i];
       one(v.x);
       one(v.y);
