@@ -83,7 +83,8 @@ int hadis_bin_hist(const double* h, const double* scores, int64_t n, int32_t n_l
  *   hfix_rows[i]            = floor(h * 2^hfix_shift)      (uint64[n])
  *   bs_rows[l/4][i][l%4]    = #{u <= s_l}  (the tau-bin)    (uint16, model quads)
  * bs_rows holds hadis_bs_store_elems(n, n_light) uint16 (light models padded
- * to a multiple of 4): one 8-byte word per record and quad of models.
+ * to a multiple of 4, quad rows of n rounded up to even records): one 8-byte
+ * word per record and quad of models.
  * row_plan (hadis_row_plan_bytes) receives the row offsets and K1's work
  * items; pass it unchanged to hadis_bin_hist_rows.  bad_records (device
  * uint32, may be NULL) counts hardness values that are NaN or outside [0, 1].

@@ -63,6 +63,9 @@ __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size
 // 8-byte store / load moves a record's bins of four models
 constexpr int kQuad = 4;
 __host__ __device__ inline int64_t n_quads(int n_light) { return (n_light + kQuad - 1) / kQuad; }
+// records per quad row, rounded up to even: every quad row starts 16-byte
+// aligned, so K1's two-record (uint4) loads stay aligned for odd n too
+__host__ __device__ inline int64_t quad_stride(int64_t n) { return (n + 1) & ~(int64_t)1; }
 
 __host__ __device__ inline RowPlan row_plan_at(void* base) {
   unsigned char* p = (unsigned char*)base;
@@ -424,7 +427,7 @@ __device__ __forceinline__ void scatter_tile(const double* __restrict__ h,
       if (kFast || key[e] != 0xffffffffu) st[key[e]] = (uint16_t)bin_s(sv[e]);
     if (qm == kQuad - 1 || l == n_light - 1) {
       __syncthreads();
-      ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * n;
+      ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * quad_stride(n);
       const uint16_t* s16 = sm.st16;
       write_out(cnt, [&](int i) {
         orow[sm.gpos[i]] = make_ushort4(s16[i], qm >= 1 ? s16[kBkTile + i] : 0,
@@ -562,7 +565,7 @@ row_hist_kernel(const uint64_t* __restrict__ hf, const uint16_t* __restrict__ bs
   for (int i = threadIdx.x; i < nm * 4 * B1s; i += blockDim.x) s_bin[i] = 0;
   __syncthreads();
   const unsigned long long base = rp.row_base[k];
-  const ushort4* bq = reinterpret_cast<const ushort4*>(bs) + (int64_t)quad * n;
+  const ushort4* bq = reinterpret_cast<const ushort4*>(bs) + (int64_t)quad * quad_stride(n);
   if (narrow) row_accumulate<true>(hf, bq, r0, r1, base, nm, s_bin, B1s);
   else row_accumulate<false>(hf, bq, r0, r1, base, nm, s_bin, B1s);
   __syncthreads();
@@ -689,7 +692,7 @@ static size_t scatter_smem(int U) {
 using namespace hadis;
 
 extern "C" int64_t hadis_bs_store_elems(int64_t n, int32_t n_light) {
-  return n <= 0 || n_light <= 0 ? 0 : n_quads(n_light) * kQuad * n;
+  return n <= 0 || n_light <= 0 ? 0 : n_quads(n_light) * kQuad * quad_stride(n);
 }
 
 extern "C" size_t hadis_row_plan_bytes(int32_t n_unique) {

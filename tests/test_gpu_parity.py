@@ -605,3 +605,21 @@ def test_brute_force_solve_matches_reference(gpu_device):
             assert case["brute"] is None and case["brute_error"] == str(exc)
             continue
         _plan_matches(plan, case["brute"], rows)
+
+
+@pytest.mark.parametrize("models,n,k", [(24, 2000, 9), (40, 801, 5)])
+def test_large_pool_matches_oracle(gpu_device, models, n, k):
+    """Large pools (276 / 780 pairs; light groups of up to 39 heavy partners, an
+    odd record count on the scalar-load path) against the oracle, bit-exact rows
+    in exact mode."""
+    from paper_2509_00642_b200 import synth
+    cat = synth.geometric_catalog(models)
+    pool = select_candidates(cat, 1e-9, 1e-9)
+    assert len(pool) == models
+    rng = np.random.default_rng(models)
+    h = rng.uniform(0.0, 1.0, n)
+    noise = rng.normal(0.0, 0.05, n)
+    thr = tuple(np.linspace(0.0, 1.0, k).tolist())
+    want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
+    got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
+    assert tuples(got) == want
