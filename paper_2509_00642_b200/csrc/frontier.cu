@@ -1647,8 +1647,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   decide_kernel<<<kNumSMs * 32, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
-  if (row_smem > 48 * 1024)
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(nobypass_kernel,
+  // always opt in: the kernel's static shared memory counts against the 48 KB
+  // default too (U = 2047 needs 49128 B dynamic + the static block-scan arrays)
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(nobypass_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem));
   nobypass_kernel<<<n_pairs, kRowThreads, row_smem, st>>>(g, pcs, kept, un, exact_cap, reqbm,
                                                           req_pair, req_cell, exact_cap, counters);

@@ -221,8 +221,8 @@ extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, 
         (unsigned long long*)hist_hsum, bad_records);
   } else {
     const size_t smem = n_unique <= kMaxSmemThr ? (size_t)n_unique * 8 : 0;
-    if (smem > 48 * 1024)
-      HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_global_kernel,
+    // opt in unconditionally: static shared memory counts against the 48 KB default
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_global_kernel,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int64_t grid = (int64_t)kNumSMs * 4;
     if (grid > blocks_needed) grid = blocks_needed;

@@ -803,8 +803,8 @@ extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs
   }
   const int B1s = (n_unique + 1) | 1;
   const size_t ksmem = (size_t)kQuad * 4 * B1s * 4;
-  if (ksmem > 48 * 1024)
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel,
+  // opt in unconditionally: static shared memory counts against the 48 KB default
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem));
   const dim3 grid((unsigned)n_quads(n_light), (unsigned)max_items);
   row_hist_kernel<<<grid, kK1Threads, ksmem, st>>>(hfix_rows, bs_rows, n, n_unique, n_light, rp,

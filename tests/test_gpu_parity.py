@@ -623,3 +623,35 @@ def test_large_pool_matches_oracle(gpu_device, models, n, k):
     want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
     got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
     assert tuples(got) == want
+
+
+@pytest.mark.parametrize("k,n", [(2047, 5001), (2600, 4001)])
+def test_max_grid_layouts_agree(gpu_device, k, n):
+    """Grids at / past the row-bucketed store's limit (2047 distinct thresholds;
+    2600 takes the global-atomic K1): both K1 layouts give the same table, in
+    (theta, tau) order, and sampled rows match numpy's cell arithmetic."""
+    from paper_2509_00642_b200.profiler import rows_from_device
+    rng = np.random.default_rng(k)
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)[:3]
+    h = rng.uniform(0.0, 1.0, n)
+    noise = rng.normal(0.0, 0.05, n)
+    thr = tuple(i / (k - 1) for i in range(k))
+    scores = light_scores(pool, h, noise)
+    tables = []
+    for layout in (("bucketed", "original") if k <= 2047 else ("original",)):
+        prof = GridProfiler(pool, h, scores, layout=layout)
+        tables.append([(r.light_id, r.heavy_id, r.theta, r.tau, r.r_light, r.r_heavy,
+                        r.fidelity_cost, r.mean_latency_s)
+                       for r in rows_from_device(prof.run(thr), pool, thr)])
+    assert all(t == tables[0] for t in tables[1:])
+    rows = tables[0]
+    assert rows
+    cost, sc = og.model_arrays(pool, h, noise)
+    ids = {v.id: v for v in pool}
+    for r in random.Random(k).sample(rows, 8):
+        lt, hv = ids[r[0]], ids[r[1]]
+        _, _, rl, rh, fid, lat = og.cell_stats(h, sc[lt.id], cost[lt.id], cost[hv.id],
+                                               lt.latency_s[1], hv.latency_s[1], r[2], r[3])
+        assert (r[4], r[5], r[7]) == (rl, rh, lat)
+        assert math.isclose(r[6], fid, rel_tol=1e-9)
