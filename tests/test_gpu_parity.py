@@ -655,3 +655,29 @@ def test_max_grid_layouts_agree(gpu_device, k, n):
                                                lt.latency_s[1], hv.latency_s[1], r[2], r[3])
         assert (r[4], r[5], r[7]) == (rl, rh, lat)
         assert math.isclose(r[6], fid, rel_tol=1e-9)
+
+
+@pytest.mark.parametrize("case", ["one_row", "two_rows_8193", "tiny_n2"])
+def test_skewed_rows_match_oracle(gpu_device, case):
+    """Row-bucketed store edge cases: every record in one theta-row (K1 splits the
+    row across CTAs: atomic flush + separate row scan), a record count just past
+    a scatter tile with five light models (two quads), two records."""
+    from paper_2509_00642_b200 import synth
+    rng = np.random.default_rng(7)
+    if case == "one_row":
+        pool = select_candidates(default_catalog(), 0.1, 0.1)
+        n = 100_000
+        h = np.full(n, 0.4321)
+    elif case == "two_rows_8193":
+        pool = select_candidates(synth.geometric_catalog(6), 1e-9, 1e-9)
+        n = 8193
+        h = rng.choice([0.25, 0.75], n)
+    else:
+        pool = select_candidates(synth.geometric_catalog(6), 1e-9, 1e-9)
+        n = 2
+        h = np.array([0.1, 0.9])
+    noise = rng.normal(0.0, 0.05, n)
+    thr = tuple(np.linspace(0.0, 1.0, 9).tolist())
+    want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
+    got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
+    assert tuples(got) == want
