@@ -681,3 +681,23 @@ def test_skewed_rows_match_oracle(gpu_device, case):
     want = og.profile_rows(pool, h, noise=noise, thresholds=thr)
     got = profile_records(pool, h, noise=noise, thresholds=thr, exact_fid=True)
     assert tuples(got) == want
+
+
+def test_odd_scores_match_oracle(gpu_device):
+    """Caller-supplied scores outside [0, 1], NaN, and exactly on thresholds: the
+    tau-bins follow numpy's `s < tau` (NaN never rejects)."""
+    rng = np.random.default_rng(12)
+    pool = select_candidates(default_catalog(), 0.1, 0.1)
+    n = 3001
+    h = rng.uniform(0.0, 1.0, n)
+    thr = tuple(np.linspace(0.0, 1.0, 11).tolist())
+    sc = {}
+    for v in pool[:-1]:
+        s = rng.uniform(-0.2, 1.2, n)
+        s[rng.integers(0, n, 50)] = np.nan
+        s[rng.integers(0, n, 200)] = rng.choice(thr, 200)
+        sc[v.id] = s
+    want = og.profile_rows(pool, h, scores=sc, thresholds=thr)
+    got = profile_records(pool, h, scores=np.stack([sc[v.id] for v in pool[:-1]]),
+                          thresholds=thr, exact_fid=True)
+    assert tuples(got) == want
