@@ -701,3 +701,17 @@ def test_odd_scores_match_oracle(gpu_device):
     got = profile_records(pool, h, scores=np.stack([sc[v.id] for v in pool[:-1]]),
                           thresholds=thr, exact_fid=True)
     assert tuples(got) == want
+
+
+def test_solve_many_past_one_launch(gpu_device):
+    """More points than one device launch takes (65535): chunked launches give the
+    same plans as the reference-order oracle on a sample, in input order."""
+    doc = load_json("planner_conftest")
+    cat = catalog_from_doc(doc["catalog"])
+    rows = rows_ns(doc["table"]["rows"])
+    pr = random.Random(3)
+    lams = [pr.uniform(0.0, 150.0) for _ in range(70_001)]
+    plans = solve_many(rows, cat, lams, None, 8, 60.0, 1.5)
+    assert len(plans) == len(lams)
+    for i in [0, 1, 65534, 65535, 65536, 70_000] + pr.sample(range(len(lams)), 14):
+        _plan_matches(plans[i], op.solve(rows, cat, lams[i], {}, 8, 60.0, 1.5), rows)
