@@ -715,3 +715,31 @@ def test_solve_many_past_one_launch(gpu_device):
     assert len(plans) == len(lams)
     for i in [0, 1, 65534, 65535, 65536, 70_000] + pr.sample(range(len(lams)), 14):
         _plan_matches(plans[i], op.solve(rows, cat, lams[i], {}, 8, 60.0, 1.5), rows)
+
+
+def test_profiler_reuse_across_grids(gpu_device):
+    """One GridProfiler, alternating threshold grids and pair subsets (plans,
+    workspaces and record stores are reused or regrown): every run equals a
+    fresh profiler's run."""
+    from paper_2509_00642_b200.profiler import pair_list
+    rng = np.random.default_rng(21)
+    pool = select_candidates(default_catalog(), 0.1, 0.1)
+    n = 20_001
+    h = rng.uniform(0.0, 1.0, n)
+    scores = light_scores(pool, h, rng.normal(0.0, 0.05, n))
+    shared = GridProfiler(pool, h, scores)
+    pairs = pair_list(pool)
+    jobs = [(tuple(i / 63 for i in range(64)), None), (tuple(i / 15 for i in range(16)), None),
+            (tuple(i / 200 for i in range(201)), pairs[2:5]), (tuple(i / 63 for i in range(64)),
+                                                                pairs[:1])]
+    for thr, prs in jobs + jobs[::-1]:
+        got = shared.run(thr, pairs=prs)
+        want = GridProfiler(pool, h, scores).run(thr, pairs=prs)
+        assert got.n_rows == want.n_rows
+        for f in ("pair", "theta_pos", "tau_pos", "r_light", "r_heavy", "fid", "lat"):
+            assert torch_equal(getattr(got, f), getattr(want, f)), f
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
