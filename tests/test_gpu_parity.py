@@ -743,3 +743,22 @@ def test_profiler_reuse_across_grids(gpu_device):
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+@pytest.mark.parametrize("workers", [0, 1, 2, 64])
+def test_planner_worker_extremes(gpu_device, workers):
+    """Worker budgets at the edges (none, one, two, more than any row needs)
+    against the oracle: same plan or the same PlannerError message."""
+    doc = load_json("planner_conftest")
+    cat = catalog_from_doc(doc["catalog"])
+    rows = rows_ns(doc["table"]["rows"])
+    for lam in (0.0, 0.3, 3.0, 40.0, 400.0):
+        for t_slo in (5.0, 60.0):
+            try:
+                want = op.solve(rows, cat, lam, {"sd35-turbo": 7.0}, workers, t_slo, 1.5)
+            except Exception as exc:          # oracle raises the reference's error text
+                with pytest.raises(PlannerError, match=str(exc).split(":")[0]):
+                    solve(rows, cat, lam, {"sd35-turbo": 7.0}, workers, t_slo, 1.5)
+                continue
+            plan = solve(rows, cat, lam, {"sd35-turbo": 7.0}, workers, t_slo, 1.5)
+            _plan_matches(plan, want, rows)
