@@ -202,6 +202,98 @@ int hadis_cascade_points(const double* h, const double* scores, int64_t n, int32
                          void* stream);
 
 /* ------------------------------------------------------------------------- */
+/* Text -> records: the record prep of profile_config        */
+/* (profiler.py:125-132) -- router.hardness (router.py:92-196), seeds          */
+/* stable_text_key / _digest / stream_normal (seeds.py:18-55).                 */
+/* ------------------------------------------------------------------------- */
+
+#define HADIS_LEX_TABLE 2048          /* open-addressing slots (power of two)   */
+#define HADIS_LEX_MAX_WORDS 1024
+#define HADIS_LEX_MAX_PHRASES 128
+#define HADIS_LEX_MAX_PHRASE_LEN 8
+#define HADIS_LEX_POOL 16384
+#define HADIS_LEX_MAX_WORD_BYTES 64
+
+enum hadis_lex_flag {                 /* hadis_lexicon.word_flags bits           */
+  HADIS_LEX_DETERMINER = 1,           /* noun_markers.txt                        */
+  HADIS_LEX_ADJECTIVE = 2,            /* adjectives.txt                          */
+  HADIS_LEX_ABSTRACT = 4,             /* abstract_nouns.txt                      */
+  HADIS_LEX_ACTION = 8,               /* action_verbs.txt                        */
+  HADIS_LEX_FREQ = 16                 /* word_frequency.tsv (rarity[] is valid)  */
+};
+
+/* Router lexicons (router.load_lexicons, router.py:64-87) as one flat image,
+ * built on the host by paper_2509_00642_b200.text.Lexicon and copied to the
+ * device once.  Words are the lowered forms tokens are compared with
+ * (router.py:157-172); `table` maps FNV-1a-32(word bytes) & (TABLE-1) by
+ * linear probing to a word id (-1 = empty).  rarity[w] is router._rarity(w)
+ * (router.py:107-114, evaluated with the host libm at build time).  Spatial
+ * phrases (as word ids) are grouped by first word in the reference's scan
+ * order (longest first, then lexicographic; router.py:71-76, 134-151). */
+typedef struct hadis_lexicon {
+  double rarity[HADIS_LEX_MAX_WORDS];
+  int32_t n_words, n_phrases, max_phrase_len, max_word_bytes;
+  int16_t table[HADIS_LEX_TABLE];
+  uint16_t word_off[HADIS_LEX_MAX_WORDS];
+  uint16_t phrase_begin[HADIS_LEX_MAX_WORDS];
+  uint8_t phrase_count[HADIS_LEX_MAX_WORDS];
+  uint8_t word_len[HADIS_LEX_MAX_WORDS];
+  uint8_t word_flags[HADIS_LEX_MAX_WORDS];
+  uint8_t phrase_len[HADIS_LEX_MAX_PHRASES];
+  int16_t phrase_words[HADIS_LEX_MAX_PHRASES][HADIS_LEX_MAX_PHRASE_LEN];
+  char pool[HADIS_LEX_POOL];
+} hadis_lexicon;
+
+/* sizeof(hadis_lexicon), for bindings that build the image themselves. */
+size_t hadis_lexicon_bytes(void);
+
+/* Prompts are UTF-8 byte strings: text i = text_bytes[offsets[i] .. offsets[i+1]).
+ *
+ * hadis_text_records -- the whole record prep of profile_config:
+ *   key[i]   = SHA-256(text)[0:8] big-endian >> 1           (stable_text_key)
+ *   order    = stable ascending sort of the keys             (profiler.py:125)
+ * and, in that sorted order (out index j <-> input prompt order_out[j]):
+ *   key_out[j], h_out[j] = router.hardness(text, weights)    (router.py:192-196)
+ *   u1_out[j], u2_out[j] = the two uniforms of stream_normal(seed, key, channel)
+ *       (seeds.py:38-46): d = BLAKE2b-128(seed_part | "i" key_be64 "\x1f" |
+ *       channel_part); u1 = (d[0:8] + 1.0) / 2^64, u2 = d[8:16] / 2^64.
+ *       seed_part / channel_part are the already-packed _digest parts
+ *       (seeds.py:18-30, including their "\x1f").
+ *   raw_out[j][8] (optional) = router.raw_features in FEATURE_NAMES order.
+ * weights: device double[8] (router.check_weights already applied).
+ * Box-Muller itself is hadis_keyed_normal_host (libm, see below).
+ * The workspace (hadis_text_workspace_bytes) holds the unsorted keys and the
+ * radix-sort scratch. */
+size_t hadis_text_workspace_bytes(int64_t n_prompts);
+int hadis_text_records(const uint8_t* text_bytes, const int64_t* offsets, int64_t n,
+                       const hadis_lexicon* lexicon, const double* weights,
+                       const uint8_t* seed_part, int32_t seed_len,
+                       const uint8_t* channel_part, int32_t channel_len,
+                       int64_t* order_out, uint64_t* key_out, double* h_out, double* u1_out,
+                       double* u2_out, double* raw_out, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* router.raw_features / features / hardness for every prompt in input order
+ * (order = NULL) or in the order given (out[j] <-> prompt order[j]); any of
+ * h_out / raw_out ([n][8]) / feat_out ([n][8]) may be NULL. */
+int hadis_text_features(const uint8_t* text_bytes, const int64_t* offsets, int64_t n,
+                        const hadis_lexicon* lexicon, const double* weights,
+                        const int64_t* order, double* h_out, double* raw_out, double* feat_out,
+                        void* stream);
+
+/* stable_text_key of every prompt (input order). */
+int hadis_text_keys(const uint8_t* text_bytes, const int64_t* offsets, int64_t n,
+                    uint64_t* key_out, void* stream);
+
+/* HOST pointers.  out[i] = sigma * sqrt(-2.0 * log(u1[i])) * cos(2.0 * pi * u2[i])
+ * evaluated left to right with the process's libm -- the same log/cos/sqrt
+ * CPython's math module calls in seeds.stream_normal (seeds.py:44-46), so the
+ * noise is bit-identical to the reference on the machine it runs on (GPU
+ * libdevice log/cos are not the glibc functions).  threads <= 0: all cores. */
+int hadis_keyed_normal_host(const double* u1, const double* u2, int64_t n, double sigma,
+                            double* out, int32_t threads);
+
+/* ------------------------------------------------------------------------- */
 /* Router weight sweep (router.py:199-234)                      */
 /* ------------------------------------------------------------------------- */
 

@@ -53,6 +53,15 @@ _SIGNATURES = {
     "hadis_cascade_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
     "hadis_cascade_points": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_i32, _c_i32,
                                       _c_vp, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+    "hadis_lexicon_bytes": (_c_sz, []),
+    "hadis_text_workspace_bytes": (_c_sz, [_c_i64]),
+    "hadis_text_records": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_i32, _c_vp,
+                                    _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
+                                    _c_sz, _c_vp]),
+    "hadis_text_features": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
+                                     _c_vp, _c_vp]),
+    "hadis_text_keys": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp]),
+    "hadis_keyed_normal_host": (_c_int, [_c_vp, _c_vp, _c_i64, _c_dbl, _c_vp, _c_i32]),
     "hadis_tune_weights": (_c_int, [_c_vp, _c_vp, _c_i32, _c_i32, _c_vp, _c_i32, _c_i32, _c_vp,
                                     _c_vp, _c_vp]),
     "hadis_pareto_workspace_bytes": (_c_sz, [_c_i64]),

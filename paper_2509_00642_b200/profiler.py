@@ -18,12 +18,13 @@ Added array-level entry points (no text needed):
 * ``GridProfiler`` -- keeps records resident in HBM and runs the device
   pipeline (K1 histogram, K2 scan, K3/K4 frontier) without host round trips.
 
-What runs where: text -> hardness / keyed noise stays on the host with the
-reference's own functions (the router and seeds modules of cascadesim, which
-a cascadesim user already has); scores are formed with the reference's numpy
-expression; everything from the records onward -- bypass/reject counting,
-every grid cell, the Pareto extraction and the (theta, tau) merge -- runs in
-libhadis_b200.so on the GPU.
+What runs where: text -> records (SHA-256 keys, key sort, tokenizer,
+lexicon features, hardness, the BLAKE2b noise digest) runs on the GPU
+(text.py / csrc/text.cu) with Box-Muller's log/cos on the host libm;
+scores are formed with the reference's numpy expression; everything from
+the records onward -- bypass/reject counting, every grid cell, the Pareto
+extraction and the (theta, tau) merge -- runs in libhadis_b200.so on the
+GPU.  The reference package is not needed at run time.
 """
 
 from __future__ import annotations
@@ -37,6 +38,7 @@ import numpy as np
 
 from . import _lib
 from .catalog import catalog_hash, select_candidates
+from .text import check_weights, prompts_hash_sorted, text_records
 
 THRESHOLD_GRID = tuple(i / 10 for i in range(11))
 DEFAULT_NOISE_SIGMA = 0.05
@@ -655,22 +657,6 @@ def profile_records(pool_or_catalog, h, scores=None, noise=None, thresholds=THRE
     return CascadeTable(rows=rows, provenance=provenance)
 
 
-def _text_records(texts, seed, noise_sigma, weights):
-    """Hardness + keyed noise per prompt with the reference's own host functions."""
-    try:
-        from cascadesim import router
-        from cascadesim.seeds import stream_normal
-    except ImportError as exc:  # pragma: no cover - depends on the user's install
-        raise ImportError("profile_config on prompt text needs cascadesim's router/seeds "
-                          "(text -> hardness); use profile_records with precomputed "
-                          "records otherwise") from exc
-    lex = router.load_lexicons()
-    h = np.array([router.hardness(t, weights, lex) for t in texts], dtype=np.float64)
-    noise = np.array([stream_normal(seed, stable_text_key(t), "disc", sigma=noise_sigma)
-                      for t in texts], dtype=np.float64)
-    return h, noise
-
-
 def profile_config(catalog, prompts, seed: int = 0, noise_sigma: float = DEFAULT_NOISE_SIGMA,
                    eps_latency: float = 0.1, eps_quality: float = 0.1,
                    thresholds=THRESHOLD_GRID, weights=None, exact_fid: bool = True) -> CascadeTable:
@@ -679,14 +665,17 @@ def profile_config(catalog, prompts, seed: int = 0, noise_sigma: float = DEFAULT
     ``exact_fid`` (default True) recomputes every emitted row's fidelity with
     the numpy-exact emulation so the returned table equals the reference's
     bit for bit; False keeps the fixed-point fidelity (within ~1e-12 relative)."""
-    if not prompts:
+    texts = list(prompts)
+    if not texts:
         raise ProfileError("profile_config: empty prompt population")
     pool = _pool_of(catalog, eps_latency, eps_quality)
     thr = tuple(float(t) for t in thresholds)
-    texts = sorted(prompts, key=stable_text_key)
-    h, noise = _text_records(texts, seed, noise_sigma, weights)
-    prov = TableProvenance(catalog_hash=catalog_hash(catalog), prompts_hash=prompts_hash(texts),
-                           n_prompts=len(texts), seed=seed, noise_sigma=noise_sigma,
-                           thresholds=thr, eps_latency=eps_latency, eps_quality=eps_quality)
-    return profile_records(pool, h, scores=light_scores(pool, h, noise), thresholds=thr,
-                           exact_fid=exact_fid, provenance=prov)
+    weights = None if weights is None else check_weights(weights)
+    rec = text_records(texts, seed, noise_sigma, weights)
+    texts = [texts[i] for i in rec.order.tolist()]
+    prov = TableProvenance(catalog_hash=catalog_hash(catalog),
+                           prompts_hash=prompts_hash_sorted(texts), n_prompts=len(texts),
+                           seed=seed, noise_sigma=noise_sigma, thresholds=thr,
+                           eps_latency=eps_latency, eps_quality=eps_quality)
+    return profile_records(pool, rec.d_h, scores=light_scores(pool, rec.h, rec.noise),
+                           thresholds=thr, exact_fid=exact_fid, provenance=prov)

@@ -3,11 +3,12 @@
 
 ``tune_weights(corpus, levels)`` keeps the reference's signature, return value
 ``(weights, threshold, balanced_acc)`` and error (``RouterError`` on a
-degenerate corpus).  Text -> feature vectors stays on the host with the
-reference's own ``router.features`` (string processing, like hardness in
-``profile_config``); ``tune_weights_features`` takes the feature matrix
-directly.  Every normalized weight vector is scored on the device
-(``hadis_tune_weights``: one CTA per vector, numpy-exact scores, sort, best
+degenerate corpus).  Text -> feature vectors runs on the GPU
+(``text.text_features``: tokenizer + lexicon features, router.py:92-179);
+``tune_weights_features`` takes a feature matrix directly.  The per-text
+drop-ins ``raw_features`` / ``features`` / ``hardness`` / ``check_weights``
+(router.py:154-196) and the batched ``hardness_many`` use the same kernel.
+Every normalized weight vector is scored on the device (``hadis_tune_weights``: one CTA per vector, numpy-exact scores, sort, best
 threshold); the reference's sequential "first unless better by 1e-12" rule
 then picks the winner on the host over the per-vector results.
 """
@@ -19,10 +20,38 @@ import itertools
 import numpy as np
 
 from . import _lib
+from .text import (DEFAULT_WEIGHTS, FEATURE_CAPS, FEATURE_NAMES, RouterError,  # noqa: F401
+                   check_weights, lexicon, text_features)
 
 
-class RouterError(ValueError):
-    pass
+def load_lexicons():
+    """The packed reference lexicons (router.load_lexicons, router.py:64-87)."""
+    return lexicon()
+
+
+def raw_features(text: str, lex=None) -> dict:
+    """router.raw_features (router.py:154-172): uncapped values by feature name."""
+    raw, _, _ = text_features([text])
+    return {name: float(v) for name, v in zip(FEATURE_NAMES, raw[0].tolist())}
+
+
+def features(text: str, lex=None) -> tuple:
+    """router.features (router.py:175-179)."""
+    _, feat, _ = text_features([text])
+    return tuple(feat[0].tolist())
+
+
+def hardness(text: str, weights=None, lex=None) -> float:
+    """router.hardness (router.py:192-196)."""
+    weights = None if weights is None else check_weights(weights)
+    _, _, h = text_features([text], weights)
+    return float(h[0])
+
+
+def hardness_many(texts, weights=None):
+    """router.hardness of every text (one kernel launch), float64[n]."""
+    weights = None if weights is None else check_weights(weights)
+    return text_features(list(texts), weights)[2]
 
 
 def _weight_grid(n_features, levels):
@@ -70,11 +99,5 @@ def tune_weights(corpus, levels=(0.0, 1.0, 2.0)):
     labels = np.array([int(label) for _, label in corpus], dtype=bool)
     if len(corpus) < 2 or labels.all() or not labels.any():
         raise RouterError("degenerate-corpus: need both hard and easy examples")
-    try:
-        from cascadesim import router as text_router
-    except ImportError as exc:  # pragma: no cover - depends on the user's install
-        raise ImportError("tune_weights on prompt text needs cascadesim's router.features "
-                          "(text -> features); use tune_weights_features otherwise") from exc
-    lex = text_router.load_lexicons()
-    mat = np.array([text_router.features(text, lex) for text, _ in corpus])
+    _, mat, _ = text_features([text for text, _ in corpus])
     return tune_weights_features(mat, labels, levels)

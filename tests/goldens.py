@@ -53,3 +53,17 @@ PROFILE_CASES = ("ties3000", "geo8", "cross1500")
 
 def frontier_cases():
     return {d["name"]: d for d in load_json("frontier")}
+
+
+_TEXT = None
+
+
+def load_text():
+    """tests/golden/text.json.gz (generator: tests/golden/make_golden_text.py)."""
+    global _TEXT
+    if _TEXT is None:
+        import gzip
+        with gzip.open(os.path.join(GOLDEN, "text.json.gz"), "rt", encoding="utf-8") as fh:
+            _TEXT = json.load(fh)
+    return _TEXT
+
