@@ -125,9 +125,10 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
-def stream_handle(stream=None):
+def stream_handle(stream=None, device=None):
+    """cudaStream_t of ``stream``, else of the current stream of ``device``."""
     torch = torch_cuda()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
 
 

@@ -29,6 +29,8 @@
 #include <cfloat>
 #include <cmath>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "pairwise.cuh"
 
@@ -1225,6 +1227,46 @@ sort_requests_kernel(const unsigned long long* __restrict__ counters_ro, int64_t
   }
 }
 
+// Request sets larger than one CTA's bitonic sort (exact_cap > kSortMax):
+// (pair, cell) keys padded with ~0 past the request count, CUB radix sort
+// over the whole capacity (graph-capturable: the size is the capacity).
+__global__ void pack_requests_kernel(const unsigned long long* __restrict__ counters_ro,
+                                     int64_t rcap, int64_t cells,
+                                     const uint32_t* __restrict__ req_pair,
+                                     const uint32_t* __restrict__ req_cell,
+                                     const double* __restrict__ req_fid,
+                                     unsigned long long* __restrict__ kin,
+                                     double* __restrict__ vin) {
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rcap;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    kin[i] = i < nr ? (unsigned long long)req_pair[i] * cells + req_cell[i] : ~0ull;
+    vin[i] = i < nr ? req_fid[i] : 0.0;
+  }
+}
+
+__global__ void unpack_requests_kernel(const unsigned long long* __restrict__ counters_ro,
+                                       int64_t rcap, int64_t cells,
+                                       const unsigned long long* __restrict__ kout,
+                                       const double* __restrict__ vout, uint32_t* req_pair,
+                                       uint32_t* req_cell, double* req_fid) {
+  const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    req_pair[i] = (uint32_t)(kout[i] / cells);
+    req_cell[i] = (uint32_t)(kout[i] % cells);
+    req_fid[i] = vout[i];
+  }
+}
+
+static size_t request_sort_temp_bytes(int64_t ecap) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const double*)nullptr,
+                                  (double*)nullptr, ecap, 0, 64);
+  return bytes;
+}
+
 __device__ bool lookup_exact(int64_t nr, int64_t cells, const uint32_t* req_pair,
                              const uint32_t* req_cell, const double* req_fid, int p,
                              uint32_t cell, double* out) {
@@ -1246,7 +1288,8 @@ __device__ bool lookup_exact(int64_t nr, int64_t cells, const uint32_t* req_pair
 
 __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
                                const unsigned long long* __restrict__ counters_ro, int64_t cap,
-                               int64_t ucap, int64_t rcap, Uncertain un, Cands grp,
+                               int64_t ucap, int64_t rcap, int64_t sort_max, Uncertain un,
+                               Cands grp,
                                const unsigned long long* __restrict__ boff,
                                const uint32_t* __restrict__ req_pair,
                                const uint32_t* __restrict__ req_cell,
@@ -1258,7 +1301,7 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
   const int64_t m = (int64_t)min((unsigned long long)cap, counters_ro[0]);
   const int64_t nr = (int64_t)min((unsigned long long)rcap, counters_ro[2]);
   const int64_t cells = (int64_t)g.U * g.U;
-  if (nr > kSortMax) {  // requests were not sorted: report, decide nothing
+  if (nr > sort_max) {  // requests were not sorted: report, decide nothing
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&counters[4], 2ull);
     return;
   }
@@ -1464,7 +1507,8 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 
 struct Layout {
   size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
-      counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell, total;
+      counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell,
+      rsort[5], rsort_bytes, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1509,6 +1553,12 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.ctsum = take(8 * (ceil_div(n_cw, 4096) + 1));
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
+  if (ecap > kSortMax) {                           // CUB request sort (see pack_requests_kernel)
+    L.rsort[0] = take(8 * ecap); L.rsort[1] = take(8 * ecap);     // keys in / out
+    L.rsort[2] = take(8 * ecap); L.rsort[3] = take(8 * ecap);     // fid in / out
+    L.rsort_bytes = request_sort_temp_bytes(ecap);
+    L.rsort[4] = take(L.rsort_bytes ? L.rsort_bytes : 1);
+  }
   L.total = at;
   return L;
 }
@@ -1667,10 +1717,28 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
                                                                         (double)n, req_fid);
     }
   }
-  sort_requests_kernel<<<1, 1024, 0, st>>>(counters, exact_cap, cells, req_pair, req_cell,
-                                           req_fid);
-  resolve_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, exact_cap, un,
-                                          grp, boff, req_pair, req_cell, req_fid, kept, counters);
+  if (exact_cap > kSortMax) {
+    unsigned long long* kin = (unsigned long long*)P(L.rsort[0]);
+    unsigned long long* kout = (unsigned long long*)P(L.rsort[1]);
+    double* vin = (double*)P(L.rsort[2]);
+    double* vout = (double*)P(L.rsort[3]);
+    const unsigned rg = (unsigned)std::min<int64_t>(ceil_div(exact_cap, 256), kNumSMs * 8);
+    pack_requests_kernel<<<rg, 256, 0, st>>>(counters, exact_cap, cells, req_pair, req_cell,
+                                            req_fid, kin, vin);
+    size_t tb = L.rsort_bytes;
+    HADIS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(P(L.rsort[4]), tb, kin, kout, vin, vout,
+                                                   exact_cap, 0, 64, st));
+    unpack_requests_kernel<<<rg, 256, 0, st>>>(counters, exact_cap, cells, kout, vout, req_pair,
+                                              req_cell, req_fid);
+    launches += 1;
+  } else {
+    sort_requests_kernel<<<1, 1024, 0, st>>>(counters, exact_cap, cells, req_pair, req_cell,
+                                             req_fid);
+  }
+  const int64_t sort_max = exact_cap > kSortMax ? exact_cap : kSortMax;
+  resolve_kernel<<<kNumSMs, 256, 0, st>>>(g, pcs, counters, cand_cap, exact_cap, exact_cap,
+                                          sort_max, un, grp, boff, req_pair, req_cell, req_fid,
+                                          kept, counters);
   HADIS_LAUNCH_CHECK();
   const int n_chunks = (int)ceil_div(words_per_pair, kEmitWords);
   const int64_t n_cw = (int64_t)n_chunks * n_pairs;

@@ -8,7 +8,9 @@
 //   _solve_over_rows  :151-167 min (fidelity, total, path, row index)
 //   fallback_plan     :170-214 max bottleneck capacity over worker splits,
 //                              key (-capacity, L_light[1], L_heavy[1], row index)
-//   solve             :217-227 negative demand -> PlannerError
+//   solve             :217-227 negative demand -> PlannerError (host wrapper;
+//                              the search itself takes any demand, like
+//                              _solve_over_rows / fallback_plan do)
 // One thread evaluates one (point, row) -- all batch combos -- and CTAs reduce
 // to a per-(point, CTA) best; a second kernel reduces the CTA partials.  All
 // float64 operations are the reference's, in its order, without FMA.
@@ -110,6 +112,11 @@ __device__ __forceinline__ double path_latency(const PlanIn& in, const RowShape&
   return path;
 }
 
+// _evaluate_row (planner.py:113-148).  The drains and each model's worker
+// count depend on the batch of that model only, so they are evaluated once per
+// row (two drains) and once per batch size (min_workers), not once per combo;
+// every value is the same float64 operation on the same operands as the
+// reference's per-combo recomputation.
 __device__ Best eval_row(const PlanIn& in, int p, int r) {
   Best best;
   best.row = -1;
@@ -117,18 +124,29 @@ __device__ Best eval_row(const PlanIn& in, int p, int r) {
   const double lamv = in.lam[p];
   const int W = in.workers[p];
   const double limit = __dadd_rn(in.t_slo[p], kSlack);
-  const int nl = s.al ? in.n_batch : 1;
-  const int nh = s.ah ? in.n_batch : 1;
+  const int nb = in.n_batch;
+  const int nl = s.al ? nb : 1;
+  const int nh = s.ah ? nb : 1;
+  const double* Q = in.queues + (int64_t)p * in.n_models;
+  const double rate_l = __dmul_rn(lamv, s.sl);
+  const double dl = drain(Q[s.ml], rate_l, in.alpha);
+  double rate_h = 0.0, dh = 0.0;
+  if (!s.single) {
+    rate_h = __dmul_rn(lamv, s.sh);
+    dh = drain(Q[s.mh], rate_h, in.alpha);
+  }
+  int64_t xh_b[kMaxBatch];
+  for (int ih = 0; ih < nh; ++ih)
+    xh_b[ih] = s.ah ? min_workers(rate_h, in.mu[s.mh * nb + ih]) : 0;
   double best_total = 0.0, best_path = 0.0;
   for (int il = 0; il < nl; ++il) {
-    int64_t xl = 0;
-    if (s.al) xl = min_workers(__dmul_rn(lamv, s.sl), in.mu[s.ml * in.n_batch + il]);
+    const int64_t xl = s.al ? min_workers(rate_l, in.mu[s.ml * nb + il]) : 0;
+    if (xl > W) continue;                             // every combo of this il is over budget
+    const double pl = __dadd_rn(0.0, __dadd_rn(in.lat[s.ml * nb + il], dl));
     for (int ih = 0; ih < nh; ++ih) {
-      int64_t xh = 0;
-      if (s.ah) xh = min_workers(__dmul_rn(lamv, s.sh), in.mu[s.mh * in.n_batch + ih]);
-      const int64_t total = xl + xh;
+      const int64_t total = xl + xh_b[ih];
       if (total > W) continue;
-      const double path = path_latency(in, s, p, il, ih, lamv);
+      const double path = s.single ? pl : __dadd_rn(pl, __dadd_rn(in.lat[s.mh * nb + ih], dh));
       if (path > limit) continue;
       const double tot = (double)total;
       if (best.row < 0 || tot < best_total || (tot == best_total && path < best_path)) {
@@ -136,7 +154,7 @@ __device__ Best eval_row(const PlanIn& in, int p, int r) {
         best_total = tot;
         best_path = path;
         best.xl = (int32_t)xl;
-        best.xh = (int32_t)xh;
+        best.xh = (int32_t)xh_b[ih];
         best.bl = il;
         best.bh = ih;
       }
@@ -217,12 +235,10 @@ solve_rows_kernel(PlanIn in, int fallback, const int32_t* __restrict__ need_fb,
   if (fallback && !need_fb[p]) return;
   Best mine;
   mine.row = -1;
-  if (in.lam[p] >= 0.0) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < in.n_rows;
-         r += gridDim.x * blockDim.x) {
-      const Best c = fallback ? fallback_row(in, p, r) : eval_row(in, p, r);
-      if (better(c, mine)) mine = c;
-    }
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < in.n_rows;
+       r += gridDim.x * blockDim.x) {
+    const Best c = fallback ? fallback_row(in, p, r) : eval_row(in, p, r);
+    if (better(c, mine)) mine = c;
   }
   block_reduce_store(mine, partial + (int64_t)p * gridDim.x + blockIdx.x);
 }
@@ -243,12 +259,6 @@ reduce_points_kernel(PlanIn in, int fallback, int nblk, const Best* __restrict__
   block_reduce_store(mine, &res);
   __syncthreads();
   if (threadIdx.x != 0) return;
-  if (in.lam[p] < 0.0) {
-    plan_row[p] = -1;
-    plan_flags[p] = 2;
-    need_fb[p] = 0;
-    return;
-  }
   if (!fallback) {
     need_fb[p] = res.row < 0;
     if (res.row < 0) return;

@@ -168,6 +168,9 @@ class DeviceRows:
         dev = self.device
         P = int(lam.shape[0])
         lib = _lib.load()
+        if torch.cuda.current_device() != dev.index and dev.index is not None:
+            with torch.cuda.device(dev):
+                return self.launch(lam, t_slo, workers, qmat, alpha, stream)
         n_rows = len(self.rows) if self.rows else self.n_rows
         ws_bytes = lib.hadis_solve_workspace_bytes(P, n_rows)
         if self._ws is None or self._ws.numel() < ws_bytes:
@@ -183,7 +186,7 @@ class DeviceRows:
             len(self.batch_sizes), p(self.d_batch), p(self.d_lat), p(self.d_mu), p(self.d_lat1), P,
             p(lam), p(t_slo), p(workers), p(qmat), float(alpha), p(out["row"]), p(out["x"]),
             p(out["b"]), p(out["path"]), p(out["flags"]), p(self._ws), ws_bytes,
-            _lib.stream_handle(stream)), "hadis_solve_many")
+            _lib.stream_handle(stream, dev)), "hadis_solve_many")
         return out
 
     def solve_arrays(self, lams, t_slos, workers, queues_list, alpha):
@@ -208,8 +211,6 @@ class DeviceRows:
 
 def _plan_from(dr: DeviceRows, res, p, lam, queues, label):
     flags = int(res["flags"][p])
-    if flags & 2:
-        raise PlannerError("solve: negative demand")
     ri = int(res["row"][p])
     if ri < 0:
         raise PlannerError("fallback: no serveable rows")
@@ -254,7 +255,16 @@ def device_rows(rows, catalog) -> DeviceRows:
 
 def solve_many(table, catalog, lams, queues=None, workers=DEFAULT_WORKERS, t_slo=DEFAULT_T_SLO_S,
                alpha=DEFAULT_QUEUE_ALPHA, label="online"):
-    """planner.solve for many points at once; scalars broadcast, lists are per point."""
+    """planner.solve for many points at once; scalars broadcast, lists are per point.
+    Like ``solve`` (planner.py:221-222), a negative demand raises PlannerError."""
+    lams = [float(x) for x in lams]
+    if any(x < 0 for x in lams):
+        raise PlannerError("solve: negative demand")
+    return _solve_points(table, catalog, lams, queues, workers, t_slo, alpha, label)
+
+
+def _solve_points(table, catalog, lams, queues, workers, t_slo, alpha, label):
+    """_solve_over_rows + fallback_plan (planner.py:151-214) per point, any demand."""
     lams = [float(x) for x in lams]
     P = len(lams)
     t_slos = [float(t_slo)] * P if np.isscalar(t_slo) else [float(x) for x in t_slo]
@@ -392,8 +402,7 @@ def fallback_plan(indexed_rows, catalog, lam, queues, workers, t_slo, alpha, lab
     rows = [r for _, r in indexed_rows]
     order = sorted(range(len(indexed_rows)), key=lambda i: indexed_rows[i][0])
     ordered = [rows[i] for i in order]
-    plan = solve_many(ordered, catalog, [lam], queues, workers, -float("inf"), alpha, label)[0]
-    return plan
+    return _solve_points(ordered, catalog, [lam], queues, workers, -float("inf"), alpha, label)[0]
 
 
 @dataclass
@@ -480,9 +489,7 @@ def proteus_plan(catalog, lam: float, queues=None, workers: int = DEFAULT_WORKER
     over one single-model row per candidate variant."""
     from .catalog import select_candidates
     rows = [_single_model_row(v) for v in select_candidates(catalog, eps_latency, eps_quality)]
-    if lam < 0:
-        raise PlannerError("solve: negative demand")
-    return solve_many(rows, catalog, [lam], queues, workers, t_slo, alpha, "proteus")[0]
+    return _solve_points(rows, catalog, [lam], queues, workers, t_slo, alpha, "proteus")[0]
 
 
 def diffserve_plan(table, catalog, lam: float, queues=None, workers: int = DEFAULT_WORKERS,
@@ -495,9 +502,7 @@ def diffserve_plan(table, catalog, lam: float, queues=None, workers: int = DEFAU
             and r.theta == max_theta]
     if not rows:
         raise PlannerError(f"diffserve_plan: table has no rows for pair {light_id}/{heavy_id}")
-    if lam < 0:
-        raise PlannerError("solve: negative demand")
-    return solve_many(rows, catalog, [lam], queues, workers, t_slo, alpha, "diffserve")[0]
+    return _solve_points(rows, catalog, [lam], queues, workers, t_slo, alpha, "diffserve")[0]
 
 
 PLANNER_MODES = ("online", "cache-d", "cache-dq", "clipper-light", "clipper-heavy", "proteus",

@@ -331,13 +331,21 @@ class GridProfiler:
         return self.finish(self.launch(self.plan(thresholds, pairs), exact_fid, stream))
 
     def launch(self, plan: ProfilePlan, exact_fid=False, stream=None, events=None):
+        """See ``_launch``; runs with ``self.device`` current (kernels and the
+        default stream belong to the profiler's device, not the caller's)."""
+        with self.torch.cuda.device(self.device):
+            return self._launch(plan, exact_fid, stream, events)
+
+    def _launch(self, plan: ProfilePlan, exact_fid=False, stream=None, events=None):
         """Enqueue B (row-bucketed record store), K1 (histogram), K2 (2-D scan)
         and K3/K4 (frontier) on ``stream``; no host synchronisation.  ``events``
         (optional list of 6 torch.cuda.Event) brackets B0-B2 | B3 | K1 | K2 | K3+K4."""
         torch = self.torch
         dev = self.device
-        st = _lib.stream_handle(stream)
+        st = _lib.stream_handle(stream, dev)
         bins = (plan.U + 1) * (plan.U + 1) * plan.n_light
+        # stream None = the current stream at launch time (a captured graph
+        # replays on whichever stream is current then, so keep None)
         state = dict(plan=plan, exact_fid=exact_fid, stream=stream,
                      scanned=torch.empty((plan.U + 1) * plan.n_light, dtype=torch.uint8,
                                          device=dev),
@@ -345,7 +353,8 @@ class GridProfiler:
                      hsum=torch.empty(bins, dtype=torch.int64, device=dev),
                      scores=self.scores[plan.slot0:plan.slot0 + plan.n_light])
         p = _lib.ptr
-        rec = (lambda i: events[i].record(stream)) if events is not None else (lambda i: None)
+        ev_stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        rec = (lambda i: events[i].record(ev_stream)) if events is not None else (lambda i: None)
         rec(0)
         if self.layout == "bucketed" and plan.U < 2048:
             hfix, bs, rplan = self._bucket_store(plan.n_light)
@@ -396,15 +405,19 @@ class GridProfiler:
 
             def capture(self):
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                with torch.cuda.device(prof.device), torch.cuda.graph(g):
                     state = prof.launch(plan, exact_fid)
+                # the graph bakes in raw pointers: own every buffer it touches
+                # (the profiler may reallocate its workspace / record store later)
                 self.graph, self.state, self.caps = g, state, plan.caps
+                self.buffers = (prof._ws, prof._store, prof.h, prof.scores, prof.bad)
 
             def launch(self):
                 """Enqueue one replay on the current stream (no host sync)."""
                 if self.caps != plan.caps:
                     self.capture()
-                self.graph.replay()
+                with torch.cuda.device(prof.device):
+                    self.graph.replay()
                 return self.state
 
             def __call__(self):
@@ -438,17 +451,18 @@ class GridProfiler:
             p(self.h), p(state["scores"]), 1 if state["exact_fid"] else 0, p(self._ws), ws_bytes,
             cand_cap, exact_cap, out_cap, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]),
             p(out["r_light"]), p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
-            _lib.stream_handle(state["stream"])), "hadis_pair_frontiers")
+            _lib.stream_handle(state["stream"], self.device)), "hadis_pair_frontiers")
         # the record-validation flag rides along, so finish() needs one device read
-        if state["stream"] is None:
+        with torch.cuda.stream(state["stream"] or torch.cuda.current_stream(self.device)):
             stats[-1:].copy_(self.bad)
-        else:
-            with torch.cuda.stream(state["stream"]):
-                stats[-1:].copy_(self.bad)
         state.update(out=out, stats=stats, caps=caps)
 
     def finish(self, state) -> DeviceTable:
         """Synchronise, check device-side status, grow capacities and rerun if needed."""
+        with self.torch.cuda.device(self.device):
+            return self._finish(state)
+
+    def _finish(self, state) -> DeviceTable:
         plan = state["plan"]
         for _ in range(6):
             dev_stats = state["stats"]
@@ -456,8 +470,10 @@ class GridProfiler:
             if pin is None or pin.numel() < dev_stats.numel():
                 pin = self._stats_pin = self.torch.empty(dev_stats.numel(),
                                                          dtype=self.torch.int64).pin_memory()
-            pin[:dev_stats.numel()].copy_(dev_stats, non_blocking=True)
-            (state["stream"] or self.torch.cuda.current_stream()).synchronize()
+            st = state["stream"] or self.torch.cuda.current_stream(self.device)
+            with self.torch.cuda.stream(st):
+                pin[:dev_stats.numel()].copy_(dev_stats, non_blocking=True)
+            st.synchronize()
             stats = pin[:dev_stats.numel()].tolist()
             if stats[-1]:
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
@@ -466,13 +482,22 @@ class GridProfiler:
             if stats[_lib.ST_OVERFLOW] & 128:
                 raise ProfileError("profile_records: more than 65 pool models per light stage "
                                    "is not supported")
-            if stats[_lib.ST_OVERFLOW] & (2 | 4 | 64):
+            if stats[_lib.ST_OVERFLOW] & 2:
                 raise ProfileError("profile_records: too many exactness-critical cells "
                                    f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
             cand_cap, exact_cap, out_cap = state["caps"]
             cells = plan.cells
-            cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
-            out_cap = int(min(cells, max(out_cap * 2, cand_cap + plan.U * plan.P)))
+            of = stats[_lib.ST_OVERFLOW]
+            if of & 16:                   # candidate list
+                cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
+            if of & (8 | 16):             # output rows (bounded by candidates + nobypass rows)
+                out_cap = int(min(cells, max(out_cap * 2, cand_cap + plan.U * plan.P,
+                                             stats[_lib.ST_ROWS] + 1)))
+            if of & (4 | 32 | 64):        # uncertain decisions / exact requests overflowed
+                need = max(stats[_lib.ST_UNCERTAIN], stats[_lib.ST_EXACT_CELLS]) + 1
+                exact_cap = int(min(cells * 2, max(exact_cap * 4, need)))
+            if (cand_cap, exact_cap, out_cap) == tuple(state["caps"]):
+                raise ProfileError(f"profile_records: capacity overflow {of:#x} cannot grow")
             plan.caps = (cand_cap, exact_cap, out_cap)
             self._frontier(state, plan.caps)
         else:
@@ -495,7 +520,13 @@ class TablePipeline:
     sweeps): host records in, host row arrays out, double-buffered so that
     the H2D copy of set i, the device build of set i-1 and the D2H copy of
     set i-2's rows run concurrently (PCIe is full duplex; the build is one
-    CUDA graph).  Every record set must have the same shape (n, light rows)."""
+    CUDA graph).  Every record set must have the same shape (n, light rows).
+
+    Rows land in pinned host buffers owned by the set's slot (two slots);
+    ``run(inputs, on_rows)`` hands each set's rows to ``on_rows(i, rows)``
+    once their copy has completed -- ``rows`` maps FIELDS to pinned tensors
+    that stay valid until the same slot's next set finishes (two sets later),
+    so the callback must consume or copy them."""
 
     FIELDS = ("pair", "theta_pos", "tau_pos", "r_light", "r_heavy", "fid", "lat")
 
@@ -507,57 +538,69 @@ class TablePipeline:
         self.torch = torch
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.slots = []
-        for _ in range(2):
-            d_h = torch.zeros(n, dtype=torch.float64, device=self.device)
-            d_sc = torch.zeros((n_rows_scores, n), dtype=torch.float64, device=self.device)
-            prof = GridProfiler(pool, d_h, d_sc, device=self.device, slots=score_slots)
-            self.slots.append(dict(h=d_h, sc=d_sc, prof=prof, plan=prof.plan(thresholds, pairs),
-                                   replay=None, ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(),
-                                   ev_out=torch.cuda.Event(), busy=False))
-        self.s_in = torch.cuda.Stream(device=self.device)
-        self.s_comp = torch.cuda.Stream(device=self.device)
-        self.s_out = torch.cuda.Stream(device=self.device)
-        self.stats_pin = [torch.zeros(_lib.ST_PAIR0 + 1, dtype=torch.int64).pin_memory()
-                          for _ in range(2)]
-        self.bad_pin = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
-        self.out_pin = {}
+        with torch.cuda.device(self.device):
+            for _ in range(2):
+                d_h = torch.zeros(n, dtype=torch.float64, device=self.device)
+                d_sc = torch.zeros((n_rows_scores, n), dtype=torch.float64, device=self.device)
+                prof = GridProfiler(pool, d_h, d_sc, device=self.device, slots=score_slots)
+                self.slots.append(dict(h=d_h, sc=d_sc, prof=prof,
+                                       plan=prof.plan(thresholds, pairs), replay=None,
+                                       ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(),
+                                       ev_out=torch.cuda.Event(), busy=False, out={},
+                                       stats_pin=torch.zeros(_lib.ST_PAIR0 + 1,
+                                                             dtype=torch.int64).pin_memory(),
+                                       bad_pin=torch.zeros(1, dtype=torch.int32).pin_memory()))
+            self.s_in = torch.cuda.Stream(device=self.device)
+            self.s_comp = torch.cuda.Stream(device=self.device)
+            self.s_out = torch.cuda.Stream(device=self.device)
 
     def warm(self, h_pin, sc_pin):
         """First build of both slots on these records (learns capacities, captures graphs)."""
-        for sl in self.slots:
-            sl["h"].copy_(h_pin)
-            sl["sc"][:sc_pin.shape[0]].copy_(sc_pin)
-            sl["replay"] = sl["prof"].graph(sl["plan"])
-        self.torch.cuda.synchronize(self.device)
+        with self.torch.cuda.device(self.device):
+            for sl in self.slots:
+                sl["h"].copy_(h_pin)
+                sl["sc"][:sc_pin.shape[0]].copy_(sc_pin)
+                sl["replay"] = sl["prof"].graph(sl["plan"])
+            self.torch.cuda.synchronize(self.device)
 
-    def _out_buffers(self, dt_state, n_rows):
-        out = dt_state["out"]
-        bufs = {}
+    def _out_buffers(self, sl, n_rows):
+        bufs = sl["out"]
         for f in self.FIELDS:
-            v = out[f]
-            buf = self.out_pin.get(f)
+            v = sl["replay"].state["out"][f]
+            buf = bufs.get(f)
             if buf is None or buf.numel() < n_rows:
-                buf = self.out_pin[f] = self.torch.empty(max(n_rows, 1), dtype=v.dtype).pin_memory()
-            bufs[f] = buf
+                bufs[f] = self.torch.empty(max(n_rows, 1), dtype=v.dtype).pin_memory()
         return bufs
 
-    def run(self, inputs):
+    def run(self, inputs, on_rows=None):
         """inputs: list of (h_pin, sc_pin) pinned host tensors.  Returns the
-        per-set (n_rows, bytes_h2d, bytes_d2h); rows land in ``out_pin``."""
+        per-set (set index, n_rows, d2h bytes); rows go to ``on_rows``."""
+        with self.torch.cuda.device(self.device):
+            return self._run(inputs, on_rows)
+
+    def _run(self, inputs, on_rows):
         torch = self.torch
         done = []
-        pending = None                                  # (slot index, step index)
+        pending = []                                    # (slot index, set index, n_rows)
 
-        def finalize(k):
+        def deliver(k, i, n_rows):
+            sl = self.slots[k]
+            sl["ev_out"].synchronize()
+            if on_rows is not None:
+                on_rows(i, {f: sl["out"][f][:n_rows] for f in self.FIELDS})
+
+        def finalize(k, i):
             sl = self.slots[k]
             sl["ev_stats"].synchronize()
-            stats = self.stats_pin[k].tolist()
-            if int(self.bad_pin[k][0]):
+            stats = sl["stats_pin"].tolist()
+            if int(sl["bad_pin"][0]):
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW]:
                 raise ProfileError("TablePipeline: capacity overflow; rebuild with warm()")
             n_rows = stats[_lib.ST_ROWS]
-            bufs = self._out_buffers(sl["replay"].state, n_rows)
+            if len(pending) == 2:                        # this slot's previous set: hand it out
+                deliver(*pending.pop(0))
+            bufs = self._out_buffers(sl, n_rows)
             nbytes = 0
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(sl["ev_comp"])
@@ -566,8 +609,10 @@ class TablePipeline:
                     bufs[f][:n_rows].copy_(v, non_blocking=True)
                     nbytes += n_rows * v.element_size()
                 sl["ev_out"].record(self.s_out)
+            pending.append((k, i, n_rows))
             return n_rows, nbytes
 
+        launched = None                                  # (slot index, set index)
         for i, (h_pin, sc_pin) in enumerate(inputs):
             k = i % 2
             sl = self.slots[k]
@@ -583,17 +628,18 @@ class TablePipeline:
                     self.s_comp.wait_event(sl["ev_out"])  # its previous rows are copied out
                 state = sl["replay"].launch()
                 sl["ev_comp"].record(self.s_comp)
-                self.stats_pin[k][:].copy_(state["stats"][:_lib.ST_PAIR0 + 1], non_blocking=True)
-                self.bad_pin[k].copy_(sl["prof"].bad, non_blocking=True)
+                sl["stats_pin"][:].copy_(state["stats"][:_lib.ST_PAIR0 + 1], non_blocking=True)
+                sl["bad_pin"].copy_(sl["prof"].bad, non_blocking=True)
                 sl["ev_stats"] = torch.cuda.Event()
                 sl["ev_stats"].record(self.s_comp)
             sl["busy"] = True
-            if pending is not None:
-                done.append((pending[1],) + finalize(pending[0]))
-            pending = (k, i)
-        if pending is not None:
-            done.append((pending[1],) + finalize(pending[0]))
-        self.s_out.synchronize()
+            if launched is not None:
+                done.append((launched[1],) + finalize(*launched))
+            launched = (k, i)
+        if launched is not None:
+            done.append((launched[1],) + finalize(*launched))
+        while pending:
+            deliver(*pending.pop(0))
         return done
 
 

@@ -472,6 +472,29 @@ def test_planner_modes_match_reference(gpu_device):
             assert plan.queues == w["queues"] and info == want["info"], (key, ep)
 
 
+def test_fallback_plan_and_negative_demand_match_reference(gpu_device):
+    """fallback_plan over explicit (index, row) pairs -- including negative
+    demand, which only ``solve`` rejects (planner.py:170-222) -- equals the
+    reference's plans field by field."""
+    from paper_2509_00642_b200.planner import PlannerError, fallback_plan, solve_many
+    from paper_2509_00642_b200.profiler import CascadeRow
+    doc = load_json("planner_conftest")
+    modes = load_json("planner_modes")
+    cat = default_catalog()
+    rows = tuple(CascadeRow(**r) for r in doc["table"]["rows"])
+    indexed = list(enumerate(rows))
+    for case in modes["fallback"]:
+        plan = fallback_plan(indexed, cat, case["lam"], dict(case["queues"]), case["workers"],
+                             30.0, 1.5, "fb")
+        w = case["plan"]
+        assert {k: getattr(plan.row, k) for k in w["row"]} == w["row"], case
+        assert (plan.workers, plan.batches, plan.infeasible, plan.label) == \
+            (w["workers"], w["batches"], w["infeasible"], w["label"]), case
+        assert plan.path_latency_s == w["path_latency_s"], case
+    with pytest.raises(PlannerError, match="solve: negative demand"):
+        solve_many(rows, cat, [1.0, -0.5])
+
+
 # ------------------------------------------------ router weight sweep (f3)
 
 @pytest.mark.parametrize("name", ["separable80", "noisy600", "noisy3000"])
@@ -530,10 +553,11 @@ def test_table_pipeline_matches_single_builds(gpu_device):
     pipe.warm(*sets[0])
     for i, (h_pin, sc_pin) in enumerate(sets):
         want = GridProfiler(pool, h_pin.numpy(), sc_pin.numpy()).run(thr)
-        got = pipe.run([(h_pin, sc_pin)])
+        rows = {}
+        got = pipe.run([(h_pin, sc_pin)], on_rows=lambda k, r: rows.update(r))
         assert got[0][1] == want.n_rows
         for f in TablePipeline.FIELDS:
-            assert torch.equal(pipe.out_pin[f][:want.n_rows], getattr(want, f).cpu()), (i, f)
+            assert torch.equal(rows[f], getattr(want, f).cpu()), (i, f)
     res = pipe.run(sets)                     # all five in flight
     assert [r[0] for r in res] == list(range(5))
 
@@ -762,3 +786,73 @@ def test_planner_worker_extremes(gpu_device, workers):
                 continue
             plan = solve(rows, cat, lam, {"sd35-turbo": 7.0}, workers, t_slo, 1.5)
             _plan_matches(plan, want, rows)
+
+
+# ------------------------------------------------ capacities, pipelines, devices
+
+def _dt_arrays(dt):
+    return {f: getattr(dt, f).cpu().numpy() for f in ("pair", "theta_pos", "tau_pos", "r_light",
+                                                      "r_heavy", "fid", "lat")}
+
+
+@pytest.mark.parametrize("name", ["ties3000", "cross1500"])
+def test_exact_capacity_grows_and_cub_request_sort(gpu_device, name):
+    """An exact-request capacity below the need grows (no 'retries exhausted'),
+    and capacities above one CTA's bitonic sort take the CUB radix-sort path;
+    both give the same table as the default capacities."""
+    doc = load_json(name)
+    rec = load_npz(name)
+    cat, pool = _golden_pool(doc)
+    sc = scores_of(rec)
+    prof = GridProfiler(pool, rec["h"], np.stack([sc[v.id] for v in pool[:-1]]))
+    plan = prof.plan(doc["thresholds"])
+    base = _dt_arrays(prof.run(doc["thresholds"]))
+    cand, _, out = plan.caps
+    plan.caps = (cand, 1, out)
+    dt = prof.finish(prof.launch(plan))
+    assert all(np.array_equal(base[k], v) for k, v in _dt_arrays(dt).items())
+    plan.caps = (cand, 8192, out)
+    dt = prof.finish(prof.launch(plan))
+    assert all(np.array_equal(base[k], v) for k, v in _dt_arrays(dt).items())
+
+
+def test_table_pipeline_delivers_every_set(gpu_device):
+    """TablePipeline: each record set's rows reach the callback (no set
+    overwrites another), equal to a one-shot build of the same records."""
+    import torch
+    from paper_2509_00642_b200.profiler import TablePipeline
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    thr = tuple(i / 31 for i in range(32))
+    sets, want = [], []
+    for seed in range(5):
+        rng = np.random.default_rng(100 + seed)
+        h = rng.uniform(0.05, 0.9, 20000)
+        sc = light_scores(pool, h, rng.normal(0.0, 0.05, 20000))
+        sets.append((torch.from_numpy(h).pin_memory(), torch.from_numpy(sc).pin_memory()))
+        want.append(_dt_arrays(GridProfiler(pool, h, sc).run(thr)))
+    pipe = TablePipeline(pool, 20000, len(pool) - 1, thr)
+    pipe.warm(*sets[0])
+    got = {}
+    res = pipe.run(sets, on_rows=lambda i, rows: got.__setitem__(
+        i, {f: v.numpy().copy() for f, v in rows.items()}))
+    assert [r[0] for r in res] == list(range(5))
+    for i in range(5):
+        assert all(np.array_equal(want[i][f], got[i][f]) for f in want[i]), i
+
+
+def test_graph_replay_survives_workspace_reallocation(gpu_device):
+    """A captured replay keeps its own buffers: a later, larger run on the same
+    profiler (new workspace) does not corrupt the replay's results."""
+    cat = default_catalog()
+    pool = select_candidates(cat, 0.1, 0.1)
+    rng = np.random.default_rng(5)
+    h = rng.uniform(0.05, 0.9, 30000)
+    sc = light_scores(pool, h, rng.normal(0.0, 0.05, 30000))
+    prof = GridProfiler(pool, h, sc)
+    small = tuple(i / 15 for i in range(16))
+    replay = prof.graph(prof.plan(small))
+    want = _dt_arrays(replay())
+    prof.run(tuple(i / 200 for i in range(201)))       # bigger grid: reallocates workspace
+    got = _dt_arrays(replay())
+    assert all(np.array_equal(want[k], v) for k, v in got.items())
