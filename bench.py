@@ -6,9 +6,11 @@ One step = one full Pareto-table build of the configured workload on device-
 resident synthetic records: B row-bucketed record store (every record array
 read once), K1 2-D histogram, K2 2-D scan, K3/K4 cell
 evaluation + exact Pareto frontier + (theta, tau) merge.  For N > 1 every rank
-builds its own contiguous pair shard with no data-path collective (SPEC.md:309-310:
-pairs are independent; the table is the rank-ordered concatenation, merged once
-outside the timed region by one NCCL all-gather).  value = configs/s =
+builds its light-model-group pair shard with no data-path collective
+(pairs are independent) straight into a fixed-size slab, and
+every step ends with one NCCL all-gather of the slabs plus the merge kernel
+that writes the canonical table on every rank (inside the timed region).
+value = configs/s =
 n_pairs * K^2 / t_step (whole job; max over ranks).  Inputs (1.28 GB at c4)
 exceed the 126 MB L2, so consecutive steps stream from HBM.
 
@@ -212,8 +214,7 @@ def run_ours(args, cfg):
 
     from paper_2509_00642_b200 import _lib, synth
     from paper_2509_00642_b200.profiler import GridProfiler, pair_list
-    from paper_2509_00642_b200.sharding import (FIELDS, gather_rows, shard_light_groups,
-                                                shard_pairs)
+    from paper_2509_00642_b200.sharding import FIELDS, ShardedTable, shard_light_groups
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -235,56 +236,72 @@ def run_ours(args, cfg):
     h_pin = torch.from_numpy(h).pin_memory()
     d_h = h_pin.to(dev)
     # pinned host copies for the e2e leg; resident device copies for `value`
+    sharded = None
     if world > 1:
         # whole light-model groups per rank; the rank holds only its light
-        # models' score rows (compact, slot-mapped)
-        offset, mine = shard_light_groups(pairs, world, rank)
+        # models' score rows (compact, slot-mapped).  Every step = local build
+        # (CUDA graph) + one all-gather of the fixed-size slabs + the merge
+        # kernel: the timed value includes the merge.
+        ids, mine = shard_light_groups(pairs, world, rank)
         slots = sorted({i for i, _ in mine}) if mine else [0]
         sc_pin = torch.from_numpy(np.ascontiguousarray(scores[slots])).pin_memory()
         d_sc = sc_pin.to(dev)
-        prof = GridProfiler(pool, d_h, d_sc, device=dev, slots=slots)
+        sharded = ShardedTable(pool, d_h, d_sc, thr, dist, device=dev, slots=slots)
+        prof, plan = sharded.prof, sharded.plan
     else:
-        offset, mine = shard_pairs(pairs, world, rank)
+        mine = pairs
         sc_pin = torch.from_numpy(np.ascontiguousarray(scores)).pin_memory()
         d_sc = sc_pin.to(dev)
         prof = GridProfiler(pool, d_h, d_sc, device=dev)
-    plan = prof.plan(thr, pairs=mine) if mine else None
+        plan = prof.plan(thr)
     stream = torch.cuda.current_stream()
 
-    replay = prof.graph(plan) if plan is not None else None   # one CUDA graph per step
+    replay = prof.graph(plan) if (plan is not None and sharded is None) else None
 
     def step(events=None):
-        if plan is None:
-            arrays = {f: torch.empty(0, dtype=torch.float64, device=dev) for f in FIELDS}
-        else:
+        if sharded is not None:
             if events is None:
-                dt = replay()
-            else:                                     # eager launch, per-stage CUDA events
-                dt = prof.finish(prof.launch(plan, stream=stream, events=events))
-            arrays = {f: getattr(dt, f) for f in FIELDS}
-        return arrays                          # N > 1: this rank's pair shard, no collective
+                return sharded.step()
+            dt = prof.finish(prof.launch(plan, stream=stream, events=events)) \
+                if plan is not None else None
+            return {f: getattr(dt, f) for f in FIELDS} if dt is not None else {}
+        if events is None:
+            dt = replay()
+        else:                                     # eager launch, per-stage CUDA events
+            dt = prof.finish(prof.launch(plan, stream=stream, events=events))
+        return {f: getattr(dt, f) for f in FIELDS}
 
     for _ in range(args.warmup):
         last = step()
     rows = int(last["pair"].shape[0])
-    if world > 1:
-        # the table is the rank-ordered concatenation of the shards: check the
-        # merge once (outside the timed region) and count the rows
-        merged = gather_rows(torch, dist, last, offset, dev)
-        rows = int(merged["pair"].shape[0])
-        del merged
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    merge_info = None
+    if sharded is not None:                       # merge kernel alone (CUDA events), once
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sharded.merge()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        merge_info = {"collective": "all_gather_into_tensor of fixed-size slabs (row counts in "
+                                    "the slab header: no count round trip)",
+                      "slab_bytes": sharded.slab.nbytes, "rows_capacity": sharded.slab.cap,
+                      "bytes_received_per_rank": sharded.gather_bytes,
+                      "row_bytes": 44, "merge_kernel_ms": e0.elapsed_time(e1)}
+
     # ---- per-stage CUDA events (eager launches, same work) for stage_ms / roofline
     kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     launches0 = _lib.load().hadis_kernel_launches()
-    for s in range(args.steps):
-        step(kev[s] if plan is not None else None)
+    if plan is not None:                          # local eager builds only (no collective)
+        for s in range(args.steps):
+            step(kev[s])
     launches = (_lib.load().hadis_kernel_launches() - launches0) // max(1, args.steps)
+    if sharded is not None:
+        launches += 2                             # + the two merge kernels per step
     barrier()
 
     # ---- timed region: device resident records, one CUDA-graph replay per step
@@ -303,6 +320,7 @@ def run_ours(args, cfg):
     def stage(a, b):
         return statistics.mean([ev[a].elapsed_time(ev[b]) for ev in kev]) if plan is not None \
             else 0.0
+
     ms_plan, ms_b, ms_k1, ms_k2, ms_k34 = (stage(0, 1), stage(1, 2), stage(2, 3), stage(3, 4),
                                            stage(4, 5))
 
@@ -325,7 +343,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         e2e_ms = [(time.perf_counter() - t0) * 1e3 / e2e_steps]
         d2h = res[-1][2]
-        if res[-1][1] != int(last["pair"].shape[0]):
+        if world == 1 and res[-1][1] != int(last["pair"].shape[0]):
             raise RuntimeError(f"e2e pipeline produced {res[-1][1]} rows, expected "
                                f"{int(last['pair'].shape[0])}")
     else:
@@ -368,8 +386,8 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "models": cfg.n_models, "pairs": cfg.n_pairs,
                        "queries": n, "thresholds": cfg.k, "cells": cfg.cells, "rows": rows,
-                       "parallelism": f"pair-shard x{world}, no data-path collective" if world > 1
-                       else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
+                       "parallelism": f"pair-shard x{world} + one all-gather merge per step"
+                       if world > 1 else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
             "table_build_ms": ms_max,
             # per-stage CUDA events of an eager launch; the eager frontier span also
             # holds host launch gaps, so the in-graph frontier time is derived too
@@ -394,9 +412,11 @@ def run_ours(args, cfg):
             line["allocation_search"] = measure_allocation(torch, dev, args.steps)
             line["cascade_depth"] = measure_cascade(torch, dev, args.steps)
             line["router_sweep"] = measure_router(torch, dev, args.steps)
-        traffic = _ncu_traffic(cfg.name)
+        traffic = _ncu_traffic(cfg.name, world, L_g)
         if traffic:
             line["roofline"]["traffic"] = traffic
+        if merge_info is not None:
+            line["merge"] = merge_info
         if world == 1 and not args.no_cpu_baseline:
             v, done, secs = cpu_cells_per_s(cfg, pool, h, scores, args.cpu_seconds, 1)
             line["cpu_baseline"] = {"value": v, "unit": "configs/s", "cores": 1, "kind": "port",
@@ -585,13 +605,17 @@ def measure_router(torch, dev, steps, cpu_vectors=12):
             "cpu_vectors_sampled": cpu_vectors}
 
 
-def _ncu_traffic(name):
+def _ncu_traffic(name, world, n_light):
+    """ncu dram bytes of one B3 launch, measured for this config at this rank-0
+    light-model count (profiles/ncu_traffic.json, key "<config>/L<n_light>");
+    None when that launch shape was never captured (e.g. a multi-GPU shard)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(name)
+            doc = json.load(fh)
     except (OSError, ValueError):
         return None
+    return doc.get(f"{name}/L{n_light}")
 
 
 def main():

@@ -202,6 +202,36 @@ int hadis_cascade_points(const double* h, const double* scores, int64_t n, int32
                          void* stream);
 
 /* ------------------------------------------------------------------------- */
+/* Multi-GPU merge of pair-sharded tables (SURVEY §8 e)     */
+/* ------------------------------------------------------------------------- */
+
+/* A rank's "slab": int64 header[hdr_words] then the seven row columns of
+ * hadis_pair_frontiers at native width -- pair, theta_pos, tau_pos (int32[cap]
+ * each, back to back from byte 8*hdr_words), then r_light, r_heavy, fid, lat
+ * (float64[cap] each, from the next 8-byte boundary).  The header holds the
+ * frontier's stats array for the rank's local pairs (HADIS_ST_*, per-local-pair
+ * row counts at HADIS_ST_PAIR0 + j, the record-validation flag right after
+ * them) and a host error word at hdr_words - 1.  The frontier pass writes
+ * straight into these columns (no pack step). */
+size_t hadis_shard_slab_bytes(int32_t hdr_words, int64_t cap);
+size_t hadis_shard_merge_workspace_bytes(int32_t n_pairs);
+
+/* gathered = world slabs back to back (all_gather_into_tensor of the slabs),
+ * global pair g owned by rank pair_rank[g] as its local pair pair_local[g];
+ * rank r holds rank_npairs[r] pairs.  Writes the canonical table (pairs in
+ * global order, rows of a pair in the owner's (theta, tau) order, pair column
+ * = global id) and out_stats[5] = {total rows, OR of overflow bits (8 = a slab
+ * or out_cap overflowed), OR of record flags, OR of host error words, max rows
+ * of one rank}.  Rows are copied only when all three status words are 0. */
+int hadis_shard_merge(const void* gathered, int32_t world, size_t slab_bytes, int64_t cap,
+                      int32_t hdr_words, const int32_t* pair_rank, const int32_t* pair_local,
+                      const int32_t* rank_npairs, int32_t n_pairs, int64_t out_cap,
+                      int32_t* out_pair, int32_t* out_theta_pos, int32_t* out_tau_pos,
+                      double* out_r_light, double* out_r_heavy, double* out_fid,
+                      double* out_lat, int64_t* out_stats, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
 /* Text -> records: the record prep of profile_config        */
 /* (profiler.py:125-132) -- router.hardness (router.py:92-196), seeds          */
 /* stable_text_key / _digest / stream_normal (seeds.py:18-55).                 */

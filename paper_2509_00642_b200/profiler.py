@@ -257,6 +257,34 @@ class ProfilePlan:
         self.cells = cells
 
 
+def grow_caps(plan, caps, stats, out_limit=None):
+    """Capacities after an overflow reported in ``stats`` (hadis_frontier_stat),
+    or ProfileError for the hard limits.  ``out_limit`` caps the output rows
+    (a multi-GPU slab); None = the grid's cell count."""
+    of = stats[_lib.ST_OVERFLOW]
+    if of & 128:
+        raise ProfileError("profile_records: more than 65 pool models per light stage "
+                           "is not supported")
+    if of & 2:
+        raise ProfileError("profile_records: too many exactness-critical cells "
+                           f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
+    cand_cap, exact_cap, out_cap = caps
+    cells = plan.cells
+    if of & 16:                   # candidate list
+        cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
+    if of & (8 | 16):             # output rows (bounded by candidates + nobypass rows)
+        out_cap = int(min(cells, max(out_cap * 2, cand_cap + plan.U * plan.P,
+                                     stats[_lib.ST_ROWS] + 1)))
+        if out_limit is not None:
+            out_cap = min(out_cap, out_limit)
+    if of & (4 | 32 | 64):        # uncertain decisions / exact requests overflowed
+        need = max(stats[_lib.ST_UNCERTAIN], stats[_lib.ST_EXACT_CELLS]) + 1
+        exact_cap = int(min(cells * 2, max(exact_cap * 4, need)))
+    if (cand_cap, exact_cap, out_cap) == tuple(caps):
+        raise ProfileError(f"profile_records: capacity overflow {of:#x} cannot grow")
+    return (cand_cap, exact_cap, out_cap)
+
+
 class GridProfiler:
     """Records resident in HBM + the K1..K4 device pipeline.
 
@@ -296,6 +324,7 @@ class GridProfiler:
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._stats_pin = None
         self._store = None
+        self.sink = None        # sharding.ShardSlab: emit rows into a multi-GPU slab
 
     def row_of(self, light_index: int) -> int:
         """Score row holding pool model ``light_index`` as the light stage."""
@@ -436,14 +465,18 @@ class GridProfiler:
         if self._ws is None or self._ws.numel() < ws_bytes:
             self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=self.device)
         dev = self.device
-        out = dict(pair=torch.empty(out_cap, dtype=torch.int32, device=dev),
-                   theta_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
-                   tau_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
-                   r_light=torch.empty(out_cap, dtype=torch.float64, device=dev),
-                   r_heavy=torch.empty(out_cap, dtype=torch.float64, device=dev),
-                   fid=torch.empty(out_cap, dtype=torch.float64, device=dev),
-                   lat=torch.empty(out_cap, dtype=torch.float64, device=dev))
-        stats = torch.zeros(_lib.ST_PAIR0 + P + 1, dtype=torch.int64, device=dev)  # + bad flag
+        if self.sink is not None:           # rows go straight into a multi-GPU slab
+            out, stats = self.sink.columns(out_cap), self.sink.stats(P)
+            stats.zero_()
+        else:
+            out = dict(pair=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                       theta_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                       tau_pos=torch.empty(out_cap, dtype=torch.int32, device=dev),
+                       r_light=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                       r_heavy=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                       fid=torch.empty(out_cap, dtype=torch.float64, device=dev),
+                       lat=torch.empty(out_cap, dtype=torch.float64, device=dev))
+            stats = torch.zeros(_lib.ST_PAIR0 + P + 1, dtype=torch.int64, device=dev)  # + bad
         p = _lib.ptr
         _lib.check(self.lib.hadis_pair_frontiers(
             p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(plan.d_slot),
@@ -479,26 +512,7 @@ class GridProfiler:
                 raise ProfileError("profile_records: hardness must be finite and within [0, 1]")
             if stats[_lib.ST_OVERFLOW] == 0:
                 break
-            if stats[_lib.ST_OVERFLOW] & 128:
-                raise ProfileError("profile_records: more than 65 pool models per light stage "
-                                   "is not supported")
-            if stats[_lib.ST_OVERFLOW] & 2:
-                raise ProfileError("profile_records: too many exactness-critical cells "
-                                   f"({stats[_lib.ST_EXACT_CELLS]}); reduce the grid")
-            cand_cap, exact_cap, out_cap = state["caps"]
-            cells = plan.cells
-            of = stats[_lib.ST_OVERFLOW]
-            if of & 16:                   # candidate list
-                cand_cap = int(min(cells, max(cand_cap * 4, stats[_lib.ST_CANDIDATES] + 1)))
-            if of & (8 | 16):             # output rows (bounded by candidates + nobypass rows)
-                out_cap = int(min(cells, max(out_cap * 2, cand_cap + plan.U * plan.P,
-                                             stats[_lib.ST_ROWS] + 1)))
-            if of & (4 | 32 | 64):        # uncertain decisions / exact requests overflowed
-                need = max(stats[_lib.ST_UNCERTAIN], stats[_lib.ST_EXACT_CELLS]) + 1
-                exact_cap = int(min(cells * 2, max(exact_cap * 4, need)))
-            if (cand_cap, exact_cap, out_cap) == tuple(state["caps"]):
-                raise ProfileError(f"profile_records: capacity overflow {of:#x} cannot grow")
-            plan.caps = (cand_cap, exact_cap, out_cap)
+            plan.caps = grow_caps(plan, state["caps"], stats)
             self._frontier(state, plan.caps)
         else:
             raise ProfileError("profile_records: capacity retries exhausted")

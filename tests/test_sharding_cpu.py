@@ -1,6 +1,9 @@
 """Multi-process sharding logic on CPU (gloo, world_size 2): the pair split
-covers every pair once in canonical order and the all-gather merge of
-per-rank rows reproduces the single-process row list exactly."""
+covers every pair once in canonical order; slabs laid out as the C ABI
+defines them (hadis_shard_slab_bytes) travel through the product's
+all-gather, and a numpy mirror of hadis_shard_merge over the gathered bytes
+reproduces the canonical row list exactly.  (The CUDA merge itself runs in
+the GPU test test_sharded_profile_equals_single.)"""
 
 import os
 import socket
@@ -10,7 +13,11 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2509_00642_b200.sharding import FIELDS, gather_rows, shard_light_groups, shard_pairs
+import numpy as np
+
+from paper_2509_00642_b200 import _lib
+from paper_2509_00642_b200.sharding import (FIELDS, ShardMap, all_gather_slab, shard_light_groups,
+                                            shard_pairs, slab_offsets)
 
 
 def _free_port():
@@ -51,56 +58,98 @@ def test_shard_light_groups_partition(models, world):
         assert loads == [15] * 8 and max(lights) == 2
 
 
-def _rows_for(pair_ids):
-    # deterministic fake per-pair rows: pair p has p % 3 + 1 rows
-    rows = {f: [] for f in FIELDS}
-    for p in pair_ids:
-        for k in range(p % 3 + 1):
-            rows["pair"].append(p)
-            rows["theta_pos"].append(k)
-            rows["tau_pos"].append(2 * k + 1)
-            rows["r_light"].append(p / 7.0 + k)
-            rows["r_heavy"].append(1.0 / (p + k + 1))
-            rows["fid"].append(30.0 - p * 0.01 - k / 3.0)
-            rows["lat"].append(0.5 + p + k * 1e-3)
-    return rows
+def _rows_for(g):
+    """Deterministic fake rows of global pair g: g % 3 + 1 rows."""
+    return [(k, 2 * k + 1, g / 7.0 + k, 1.0 / (g + k + 1), 30.0 - g * 0.01 - k / 3.0,
+             0.5 + g + k * 1e-3) for k in range(g % 3 + 1)]
 
 
-def _worker(rank, world, port, n_pairs, out_path, by_light=False):
+def _fake_slab(smap, rank, cap):
+    hw = smap.hdr_words
+    nbytes = _lib.load().hadis_shard_slab_bytes(hw, cap)
+    buf = np.zeros(nbytes, dtype=np.uint8)
+    hdr = buf[:8 * hw].view(np.int64)
+    offs = slab_offsets(hw, cap)
+    cols = [buf[offs[k]:offs[k] + 4 * cap].view(np.int32) for k in range(3)] + \
+        [buf[offs[3 + k]:offs[3 + k] + 8 * cap].view(np.float64) for k in range(4)]
+    r = 0
+    for j, g in enumerate(smap.rank_ids[rank]):
+        rows = _rows_for(g)
+        hdr[_lib.ST_PAIR0 + j] = len(rows)
+        for row in rows:
+            cols[0][r] = j                                   # local pair id
+            for k, v in enumerate(row):
+                cols[1 + k][r] = v
+            r += 1
+    hdr[_lib.ST_ROWS] = r
+    return buf
+
+
+def _merge_mirror(gathered, smap, cap):
+    """numpy restatement of hadis_shard_merge (csrc/shards.cu) -- test infra."""
+    hw = smap.hdr_words
+    nbytes = _lib.load().hadis_shard_slab_bytes(hw, cap)
+    offs = slab_offsets(hw, cap)
+    out = {f: [] for f in FIELDS}
+    for g in range(smap.n_pairs):
+        r, j = int(smap.pair_rank[g]), int(smap.pair_local[g])
+        slab = gathered[r * nbytes:(r + 1) * nbytes]
+        hdr = slab[:8 * hw].view(np.int64)
+        src = int(hdr[_lib.ST_PAIR0:_lib.ST_PAIR0 + j].sum())
+        cnt = int(hdr[_lib.ST_PAIR0 + j])
+        cols = [slab[offs[k]:offs[k] + 4 * cap].view(np.int32) for k in range(3)] + \
+            [slab[offs[3 + k]:offs[3 + k] + 8 * cap].view(np.float64) for k in range(4)]
+        out["pair"] += [g] * cnt
+        for k, f in enumerate(FIELDS[1:]):
+            out[f] += cols[1 + k][src:src + cnt].tolist()
+    return out
+
+
+def _worker(rank, world, port, n_models, out_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    if by_light:                                 # pairs of a 5-model pool, light-group shards
-        plist = [(i, j) for i in range(5) for j in range(i + 1, 5)][:n_pairs]
-        off, mine_pairs = shard_light_groups(plist, world, rank)
-        mine = list(off)
-        local_ids = list(range(len(mine)))
-    else:
-        pairs = list(range(n_pairs))
-        off, mine = shard_pairs(pairs, world, rank)
-        local_ids = None
-    rows = _rows_for(mine)
-    if local_ids is not None:                    # rows carry local pair ids 0..len(mine)-1
-        rows["pair"] = [mine.index(p) for p in rows["pair"]]
-    arrays = {}
-    for f in FIELDS:
-        if f in ("pair", "theta_pos", "tau_pos"):
-            t = torch.tensor(rows[f], dtype=torch.int32)
-            arrays[f] = t - off if (f == "pair" and not by_light) else t   # local pair ids
-        else:
-            arrays[f] = torch.tensor(rows[f], dtype=torch.float64)
-    merged = gather_rows(torch, dist, arrays, off, torch.device("cpu"))
+    pairs = [(i, j) for i in range(n_models) for j in range(i + 1, n_models)]
+    smap = ShardMap(pairs, world)
+    cap = 64
+    slab = torch.from_numpy(_fake_slab(smap, rank, cap))
+    gathered = torch.empty(world * slab.numel(), dtype=torch.uint8)
+    all_gather_slab(torch, dist, slab, gathered)
     if rank == 0:
-        torch.save({f: merged[f] for f in FIELDS}, out_path)
+        torch.save(_merge_mirror(gathered.numpy(), smap, cap), out_path)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_pairs,by_light", [(6, False), (7, False), (1, False), (10, True),
-                                              (7, True)])
-def test_gather_rows_gloo_world2(tmp_path, n_pairs, by_light):
+@pytest.mark.parametrize("n_models", [2, 4, 5, 8])
+def test_slab_gather_and_merge_gloo_world2(tmp_path, n_models):
     out = str(tmp_path / "merged.pt")
-    mp.spawn(_worker, args=(2, _free_port(), n_pairs, out, by_light), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), n_models, out), nprocs=2, join=True)
     merged = torch.load(out)
-    want = _rows_for(range(n_pairs))
+    n_pairs = n_models * (n_models - 1) // 2
+    want = {f: [] for f in FIELDS}
+    for g in range(n_pairs):
+        for row in _rows_for(g):
+            want["pair"].append(g)
+            for k, f in enumerate(FIELDS[1:]):
+                want[f].append(row[k])
     for f in FIELDS:
-        got = merged[f].tolist()
-        assert got == want[f], f
+        assert merged[f] == want[f], f
+
+
+@pytest.mark.parametrize("models,world", [(16, 8), (8, 3), (4, 8), (2, 1)])
+def test_shard_map_covers_every_pair_once(models, world):
+    pairs = [(i, j) for i in range(models) for j in range(i + 1, models)]
+    smap = ShardMap(pairs, world)
+    for g in range(len(pairs)):
+        r, j = smap.pair_rank[g], smap.pair_local[g]
+        assert smap.rank_ids[r][j] == g
+    assert smap.rank_npairs.sum() == len(pairs)
+    assert smap.hdr_words % 32 == 0 and smap.hdr_words >= _lib.ST_PAIR0 + len(pairs) + 2
+
+
+@pytest.mark.parametrize("cap", [0, 1, 3, 1000, 12345])
+def test_slab_layout_matches_library(cap):
+    hw = 160
+    nbytes = _lib.load().hadis_shard_slab_bytes(hw, cap)
+    offs = slab_offsets(hw, cap)
+    assert offs[0] == 8 * hw and all(o % 8 == 0 for o in offs[3:])
+    assert offs[-1] + 8 * cap <= nbytes and nbytes % 256 == 0

@@ -24,6 +24,13 @@ def main():
     pool, h, noise, scores = synth.records(cfg, seed=5)
     prof = GridProfiler(pool, h, scores)
     pairs, merged = profile_sharded(prof, cfg.thresholds, dist)
+    # the same through ShardedTable with a CUDA graph per rank, two steps
+    from paper_2509_00642_b200.sharding import ShardedTable
+    st = ShardedTable(pool, prof.h, prof.scores, cfg.thresholds, dist)
+    for _ in range(2):
+        again = st.step()
+    for f in FIELDS:
+        assert torch.equal(again[f], merged[f]), f
     if dist.get_rank() == 0:
         single = prof.run(cfg.thresholds)
         for f in FIELDS:
