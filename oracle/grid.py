@@ -60,13 +60,19 @@ def pareto_keep(lat, qual):
     return kept
 
 
-def cell_stats(h, light_score, light_cost, heavy_cost, lat_light, lat_heavy, theta, tau):
+def cell_stats(h, light_score, light_cost, heavy_cost, lat_light, lat_heavy, theta, tau,
+               bypass=None, n_bypass=None):
     """One grid cell exactly as profiler.py:146-165 computes it.
 
+    ``bypass`` / ``n_bypass`` are the per-theta values the reference computes
+    once (``bypass_at[theta]``, profiler.py:138, and ``n_bypass`` per theta
+    row, :146-147); pass them when evaluating a whole theta row.
     Returns (n_bypass, n_reject, r_light, r_heavy, fid, mean_lat)."""
     n = h.shape[0]
-    bypass = h > theta
-    n_bypass = int(bypass.sum())
+    if bypass is None:
+        bypass = h > theta
+    if n_bypass is None:
+        n_bypass = int(bypass.sum())
     reject = ~bypass & (light_score < tau)
     n_reject = int(reject.sum())
     heavy = bypass | reject
@@ -75,14 +81,22 @@ def cell_stats(h, light_score, light_cost, heavy_cost, lat_light, lat_heavy, the
     return (n_bypass, n_reject, (n - n_bypass) / n, (n_bypass + n_reject) / n, fid, lat)
 
 
+def theta_row(h, light_score, light_cost, heavy_cost, lat_light, lat_heavy, theta, taus):
+    """Every tau cell of one theta row, with the reference's per-theta hoisting
+    (profiler.py:138, 145-149)."""
+    bypass = h > theta
+    n_bypass = int(bypass.sum())
+    return [cell_stats(h, light_score, light_cost, heavy_cost, lat_light, lat_heavy, theta, tau,
+                       bypass, n_bypass) for tau in taus]
+
+
 def pair_grid(h, light, heavy, cost, score, thresholds):
     """Every (theta, tau) cell of one pair, in grid order (index = i*K + j)."""
     cells = []
     for theta in thresholds:
-        for tau in thresholds:
-            nb, nr, rl, rh, fid, lat = cell_stats(
-                h, score[light.id], cost[light.id], cost[heavy.id],
-                light.latency_s[1], heavy.latency_s[1], theta, tau)
+        for tau, (nb, nr, rl, rh, fid, lat) in zip(thresholds, theta_row(
+                h, score[light.id], cost[light.id], cost[heavy.id], light.latency_s[1],
+                heavy.latency_s[1], theta, thresholds)):
             cells.append((light.id, heavy.id, theta, tau, rl, rh, fid, lat))
     return cells
 
@@ -121,6 +135,51 @@ def profile_rows(pool, h, noise=None, thresholds=(), scores=None):
     for light, heavy in light_heavy_pairs(pool):
         cells = pair_grid(h, light, heavy, cost, scores, thresholds)
         rows.extend(pair_frontier(cells, thresholds))
+    return rows
+
+
+_PAR = None
+
+
+def _par_rows(job):
+    h, cost, scores, pairs, thresholds = _PAR
+    pi, t0, t1 = job
+    light, heavy = pairs[pi]
+    out = []
+    for theta in thresholds[t0:t1]:
+        for tau, (nb, nr, rl, rh, fid, lat) in zip(thresholds, theta_row(
+                h, scores[light.id], cost[light.id], cost[heavy.id], light.latency_s[1],
+                heavy.latency_s[1], theta, thresholds)):
+            out.append((light.id, heavy.id, theta, tau, rl, rh, fid, lat))
+    return pi, t0, out
+
+
+def profile_rows_parallel(pool, h, scores, thresholds, procs):
+    """profile_rows with the cell grid split over ``procs`` forked processes
+    (jobs = (pair, theta block)); the per-pair frontier runs in the parent.
+    Same values as profile_rows (each cell is the same numpy computation)."""
+    import multiprocessing as mp
+    global _PAR
+    thresholds = tuple(float(t) for t in thresholds)
+    h = np.asarray(h, dtype=np.float64)
+    cost = {v.id: v.base_quality_cost + v.hardness_penalty * h for v in pool}
+    scores = {k: np.asarray(s, dtype=np.float64) for k, s in scores.items()}
+    pairs = light_heavy_pairs(pool)
+    K = len(thresholds)
+    step = max(1, K // 32)
+    jobs = [(pi, t0, min(K, t0 + step)) for pi in range(len(pairs)) for t0 in range(0, K, step)]
+    _PAR = (h, cost, scores, pairs, thresholds)
+    try:
+        with mp.get_context("fork").Pool(procs) as pool_:
+            parts = pool_.map(_par_rows, jobs, chunksize=1)
+    finally:
+        _PAR = None
+    by_pair = {}
+    for pi, t0, cells in sorted(parts, key=lambda x: (x[0], x[1])):
+        by_pair.setdefault(pi, []).extend(cells)
+    rows = []
+    for pi in range(len(pairs)):
+        rows.extend(pair_frontier(by_pair[pi], thresholds))
     return rows
 
 
