@@ -159,14 +159,20 @@ def test_full_scale_completeness_probes(gpu_device, name):
             r = a + idx
             assert (rl[r], rh[r], lat[r]) == (e_rl, e_rh, e_lat), (name, p, ti, ta)
             assert math.isclose(fid[r], e_fid, rel_tol=1e-9), (name, p, ti, ta)
-        # rows ordered before the probe in the prune's (lat, fid, index) order
-        others = (tp[a:b] * K + cp[a:b]) != ti * K + ta
-        L, F = lat[a:b][others], fid[a:b][others]
-        near = np.abs(F - e_fid) <= 1e-9 * abs(e_fid)
-        if np.any(near & (L == e_lat)) or np.any(near & (L < e_lat)):
+        # rows ordered before the probe in the prune's (lat, fid, index) order.
+        # Twins -- rows with the probe's own (r_light, r_heavy), i.e. the same
+        # non-bypassed and heavy sets (duplicate theta rows / empty tau bins) --
+        # have numpy's fid exactly: equal values, ordered by grid index.
+        G = tp[a:b] * K + cp[a:b]
+        others = G != ti * K + ta
+        L, F, G = lat[a:b][others], fid[a:b][others], G[others]
+        twin = (rl[a:b][others] == e_rl) & (rh[a:b][others] == e_rh)
+        F = np.where(twin, e_fid, F)
+        near = (np.abs(F - e_fid) <= 1e-9 * abs(e_fid)) & ~twin
+        if np.any(near & (L <= e_lat)):
             ambiguous.append((p, ti, ta))                # fidelity too close to call on fid*
             continue
-        before = (L < e_lat) | ((L == e_lat) & (F < e_fid))
+        before = (L < e_lat) | ((L == e_lat) & ((F < e_fid) | (twin & (G < ti * K + ta))))
         killed = np.any(before & (F <= e_fid))
         keep = not killed
         if ti == top:                                    # theta = max sub-frontier
