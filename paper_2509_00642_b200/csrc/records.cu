@@ -28,6 +28,7 @@
 // The original-order arrays stay with the caller for the numpy-exact
 // fidelity emulation, which depends on the reference's summation order.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -490,6 +491,261 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
   }
 }
 
+// B3 (TMA-fed): the same scatter with the record arrays streamed into a
+// shared-memory ring by the bulk-copy engine instead of register prefetch.
+// One producer warp (one elected lane) issues cp.async.bulk copies of
+// kTmaChunk-record chunks -- h, then each light model's scores, tile by tile
+// -- into kTmaSlots ring slots, each completing on its "full" mbarrier; the
+// kTmaConsumers consumer threads (16 warps) wait on it, bin the chunk from
+// shared memory and release the slot with one arrive per warp on its "empty"
+// mbarrier.  Loads therefore stay in flight through the tile prologue
+// (ranks, block scan, cursor reservations) and every write-out, and no
+// record data is held in registers across phases.  Consumer-only phases
+// synchronise with a named barrier; the producer never joins them.
+#ifndef HADIS_TMA_CONSUMER_WARPS
+#define HADIS_TMA_CONSUMER_WARPS 31
+#endif
+#ifndef HADIS_TMA_PER_CHUNK
+#define HADIS_TMA_PER_CHUNK 4
+#endif
+#ifndef HADIS_TMA_SLOTS
+#define HADIS_TMA_SLOTS 3
+#endif
+constexpr int kTmaConsumers = 32 * HADIS_TMA_CONSUMER_WARPS;   // consumer threads
+constexpr int kTmaThreads = kTmaConsumers + 32;        // + the producer warp
+#ifndef HADIS_TMA_PER
+#define HADIS_TMA_PER 8
+#endif
+constexpr int kTmaPer = HADIS_TMA_PER;                 // records per consumer per tile
+constexpr int kTmaPerChunk = HADIS_TMA_PER_CHUNK;      // records per consumer per ring chunk
+constexpr int kTmaChunks = kTmaPer / kTmaPerChunk;     // chunks per record array and tile
+constexpr int kTmaChunk = kTmaPerChunk * kTmaConsumers;   // records per ring slot
+constexpr int kTmaTile = kTmaPer * kTmaConsumers;      // records per tile
+constexpr int kTmaSlots = HADIS_TMA_SLOTS;
+constexpr int kTmaBar = 1;                             // named barrier id (consumers)
+
+struct TmaSmem {
+  double* ring;               // [kTmaSlots][kTmaChunk]
+  unsigned long long* st64;   // [kTmaTile] hfix staged in row order
+  ushort4* st4;               // [kTmaTile] tau-bins of a model quad per slot (aliases st64)
+  uint32_t* gpos;             // [kTmaTile]
+  uint32_t* cnt;              // [kMaxBins]
+  uint32_t* gbase;            // [kMaxBins]
+  double* thr;                // [U + 2]
+};
+
+__device__ __forceinline__ int64_t consumer_excl_scan(int64_t v, int64_t* s_warp, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = kTmaConsumers / 32;
+  static_assert(kW <= 32, "one warp scans the warp totals");
+  int64_t incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  named_sync(kTmaBar, kTmaConsumers);
+  if (warp == 0) {
+    int64_t w = lane < kW ? s_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    s_warp[lane] = w;
+  }
+  named_sync(kTmaBar, kTmaConsumers);
+  const int64_t excl = (warp > 0 ? s_warp[warp - 1] : 0) + incl - v;
+  *total = s_warp[kW - 1];
+  named_sync(kTmaBar, kTmaConsumers);
+  return excl;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1)
+bucket_scatter_tma_kernel(const double* __restrict__ h, const double* __restrict__ scores,
+                          int64_t n, int n_light, const double* __restrict__ thr, int U,
+                          double hscale, RowPlan rp, uint64_t* __restrict__ hfix_rows,
+                          uint16_t* __restrict__ bs_rows) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kTmaSlots], empty[kTmaSlots];
+  __shared__ int64_t s_warp[32];
+  __shared__ uint32_t s_tile_n;
+  TmaSmem sm;
+  sm.ring = reinterpret_cast<double*>(smem);
+  sm.st64 = reinterpret_cast<unsigned long long*>(sm.ring + kTmaSlots * kTmaChunk);
+  sm.st4 = reinterpret_cast<ushort4*>(sm.st64);
+  sm.gpos = reinterpret_cast<uint32_t*>(sm.st64 + kTmaTile);
+  sm.cnt = sm.gpos + kTmaTile;
+  sm.gbase = sm.cnt + kMaxBins;
+  sm.thr = reinterpret_cast<double*>(sm.gbase + kMaxBins);
+  const int B1 = U + 1;
+  const int64_t chunk = (ceil_div(n, (int64_t)gridDim.x) + 1) & ~(int64_t)1;
+  const int64_t r0 = min(n, (int64_t)blockIdx.x * chunk), r1 = min(n, r0 + chunk);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaSlots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < U + 2; i += blockDim.x) sm.thr[i] = i < U ? thr[i] : INFINITY;
+  __syncthreads();
+  if (r0 >= r1) return;
+
+  if (threadIdx.x >= kTmaConsumers) {                  // ---- producer warp
+    if (threadIdx.x == kTmaConsumers) {
+      const uint64_t pol = policy_evict_first();
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int64_t t0 = r0; t0 < r1; t0 += kTmaTile) {
+        const int64_t tn = min((int64_t)kTmaTile, r1 - t0);
+        for (int a = 0; a <= n_light; ++a) {
+          const double* src = (a == 0 ? h : scores + (int64_t)(a - 1) * n) + t0;
+          for (int c = 0; c < kTmaChunks; ++c) {
+            const int64_t m = min((int64_t)kTmaChunk, tn - (int64_t)c * kTmaChunk);
+            mbar_wait(&empty[slot], ph ^ 1u);          // slot released by every consumer warp
+            if (m > 0) {
+              mbar_arrive_expect_tx(&full[slot], (uint32_t)(m * 8));
+              bulk_load(sm.ring + slot * kTmaChunk, src + (int64_t)c * kTmaChunk,
+                        (uint32_t)(m * 8), &full[slot], pol);
+            } else {
+              mbar_arrive(&full[slot]);                // empty chunk: complete the phase
+            }
+            if (++slot == kTmaSlots) { slot = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers (threads 0 .. kTmaConsumers-1)
+  const int lane = threadIdx.x & 31;
+  int slot = 0;
+  uint32_t ph = 0;
+  // record e of this consumer: chunk e / kTmaPerChunk, two adjacent records
+  // per 16-byte load
+  auto rec = [](int e) { return 2 * ((e >> 1) * kTmaConsumers + (int)threadIdx.x) + (e & 1); };
+  auto acquire = [&]() { mbar_wait(&full[slot], ph); return sm.ring + slot * kTmaChunk; };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == kTmaSlots) { slot = 0; ph ^= 1u; }
+  };
+  // uniform grids (the common case) bin with two compares; others search
+  // with the guide tables (read through L1 from the row plan)
+  const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
+  auto bin_h = [&](double x) {
+    return mode == 0 ? uniform_bin<false>(sm.thr, U, x)
+                     : plan_bin<false>(mode, sm.thr, U, rp.guide_lt, x);
+  };
+  auto bin_s = [&](double x) {
+    return mode == 0 ? uniform_bin<true>(sm.thr, U, x)
+                     : plan_bin<true>(mode, sm.thr, U, rp.guide_le, x);
+  };
+  for (int64_t t0 = r0; t0 < r1; t0 += kTmaTile) {
+    const int tn = (int)min((int64_t)kTmaTile, r1 - t0);
+    for (int i = threadIdx.x; i < B1; i += kTmaConsumers) sm.cnt[i] = 0;
+    named_sync(kTmaBar, kTmaConsumers);
+    // 1. theta-row + local rank from the two h chunks; hfix kept in registers
+    uint32_t key[kTmaPer];
+    uint64_t hf[kTmaPer];
+#pragma unroll
+    for (int c = 0; c < kTmaChunks; ++c) {
+      const double* buf = acquire();
+      double xs[kTmaPerChunk];                      // 16-byte shared loads, two records each
+#pragma unroll
+      for (int e2 = 0; e2 < kTmaPerChunk; e2 += 2) {
+        const double2 v = reinterpret_cast<const double2*>(buf)[(rec(c * kTmaPerChunk + e2) - c * kTmaChunk) >> 1];
+        xs[e2] = v.x; xs[e2 + 1] = v.y;
+      }
+#pragma unroll
+      for (int e = c * kTmaPerChunk; e < (c + 1) * kTmaPerChunk; ++e) {
+        const int r = rec(e);
+        if (r < tn) {
+          const double x = xs[e - c * kTmaPerChunk];
+          const int b = bin_h(x);
+          const uint32_t rank = atomicAdd(&sm.cnt[b], 1u);
+          key[e] = ((uint32_t)b << 16) | rank;
+          hf[e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
+        } else {
+          key[e] = 0xffffffffu;
+          hf[e] = 0;
+        }
+      }
+      release();
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    // 2. local exclusive offsets + one global reservation per non-empty row
+    {
+      const int per = (B1 + kTmaConsumers - 1) / kTmaConsumers;
+      const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+      int64_t tsum = 0;
+      for (int i = i0; i < i1; ++i) tsum += sm.cnt[i];
+      int64_t total;
+      int64_t run = consumer_excl_scan(tsum, s_warp, &total);
+      for (int i = i0; i < i1; ++i) {
+        const uint32_t c = sm.cnt[i];
+        sm.gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
+        sm.cnt[i] = (uint32_t)run;
+        run += c;
+      }
+      if (threadIdx.x == 0) s_tile_n = (uint32_t)total;
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    // 3. sorted slot, global position, hfix staged in row order
+#pragma unroll
+    for (int e = 0; e < kTmaPer; ++e) {
+      if (key[e] != 0xffffffffu) {
+        const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
+        const uint32_t s = sm.cnt[b] + rank;
+        sm.gpos[s] = sm.gbase[b] + rank;
+        sm.st64[s] = hf[e];
+        key[e] = s;
+      }
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    const int cnt = (int)s_tile_n;
+    for (int i = threadIdx.x; i < cnt; i += kTmaConsumers) hfix_rows[sm.gpos[i]] = sm.st64[i];
+    // 4. per light model: two chunks binned into the quad staging, four
+    //    models per write-out (one 8-byte store per record and quad)
+    for (int l = 0; l < n_light; ++l) {
+      const int qm = l % kQuad;
+      if (qm == 0) named_sync(kTmaBar, kTmaConsumers);   // previous write-out done
+      uint16_t* st = reinterpret_cast<uint16_t*>(sm.st4) + qm;    // lane qm of each slot
+#pragma unroll
+      for (int c = 0; c < kTmaChunks; ++c) {
+        const double* buf = acquire();
+        double xs[kTmaPerChunk];
+#pragma unroll
+        for (int e2 = 0; e2 < kTmaPerChunk; e2 += 2) {
+          const double2 v = reinterpret_cast<const double2*>(buf)[(rec(c * kTmaPerChunk + e2) - c * kTmaChunk) >> 1];
+          xs[e2] = v.x; xs[e2 + 1] = v.y;
+        }
+#pragma unroll
+        for (int e = c * kTmaPerChunk; e < (c + 1) * kTmaPerChunk; ++e)
+          if (key[e] != 0xffffffffu)
+            st[4 * key[e]] = (uint16_t)bin_s(xs[e - c * kTmaPerChunk]);
+        release();
+      }
+      if (qm == kQuad - 1 || l == n_light - 1) {
+        named_sync(kTmaBar, kTmaConsumers);
+        ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * quad_stride(n);
+        // lanes past the last model of a partial quad carry stale bins; K1
+        // reads only the quad's n_light % 4 models
+        for (int i = threadIdx.x; i < cnt; i += kTmaConsumers) orow[sm.gpos[i]] = sm.st4[i];
+      }
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+  }
+}
+
+static size_t scatter_tma_smem(int U) {
+  return (size_t)8 * kTmaSlots * kTmaChunk + (size_t)8 * kTmaTile + (size_t)4 * kTmaTile +
+         (size_t)4 * 2 * kMaxBins + (size_t)8 * (U + 2);
+}
+
 // K1: one CTA per (row chunk, model quad).  Each record's hfix (8 B) and its
 // four tau-bins (one 8-byte load) feed the four models' shared-memory row
 // histograms: count + 16-bit hardness limbs relative to the row's fixed-point
@@ -753,11 +1009,23 @@ extern "C" int hadis_records_scatter(const double* h, const double* scores, int6
   const double hscale = ldexp(1.0, hfix_shift);
   bool vec = (reinterpret_cast<uintptr_t>(h) & 15) == 0 && (n & 1) == 0 &&
              (n_light == 0 || (reinterpret_cast<uintptr_t>(scores) & 15) == 0);
+  int64_t sgrid = ceil_div(n, kBkTile);
+  if (sgrid > kNumSMs) sgrid = kNumSMs;
+  const char* legacy = getenv("HADIS_B3_REGISTER_PATH");   // A/B switch for measurements
+  if (vec && !(legacy && legacy[0] == '1')) {
+    // aligned record arrays: the TMA-fed scatter (binning mode read on the device)
+    const size_t tsmem = scatter_tma_smem(n_unique);
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_tma_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+    bucket_scatter_tma_kernel<<<(unsigned)sgrid, kTmaThreads, tsmem, st>>>(
+        h, scores, n, n_light, thr_unique, n_unique, hscale, rp, hfix_rows, bs_rows);
+    HADIS_LAUNCH_CHECK();
+    hadis_count_launches(1);
+    return HADIS_OK;
+  }
   const size_t ssmem = scatter_smem(n_unique);
   auto kern = vec ? bucket_scatter_kernel<true> : bucket_scatter_kernel<false>;
   HADIS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-  int64_t sgrid = ceil_div(n, kBkTile);
-  if (sgrid > kNumSMs) sgrid = kNumSMs;
   kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
                                                    hscale, rp, hfix_rows, bs_rows);
   HADIS_LAUNCH_CHECK();
