@@ -267,6 +267,7 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
 
     replay = prof.graph(plan) if (plan is not None and sharded is None) else None
+    last_dt = None
 
     def step(events=None):
         if sharded is not None:
@@ -279,6 +280,8 @@ def run_ours(args, cfg):
             dt = replay()
         else:                                     # eager launch, per-stage CUDA events
             dt = prof.finish(prof.launch(plan, stream=stream, events=events))
+        nonlocal last_dt
+        last_dt = dt
         return {f: getattr(dt, f) for f in FIELDS}
 
     for _ in range(args.warmup):
@@ -418,8 +421,12 @@ def run_ours(args, cfg):
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
         }
+        if world == 1:
+            line["materialise"] = measure_materialise(last_dt, pool, thr)
         if not args.no_allocation:
             line["allocation_search"] = measure_allocation(torch, dev, args.steps)
+            line["solve_call_ms"] = measure_solve_calls(torch, dev)
+            line["text_records"] = measure_text(torch, dev)
             line["cascade_depth"] = measure_cascade(torch, dev, args.steps)
             line["router_sweep"] = measure_router(torch, dev, args.steps)
         traffic = _ncu_traffic(cfg.name, world, L_g)
@@ -615,6 +622,85 @@ def measure_router(torch, dev, steps, cpu_vectors=12):
             "acc": acc, "cpu_s_per_vector": cpu_per_vec,
             "cpu_sweep_s_extrapolated": cpu_per_vec * len(grid), "cpu_kind": "port",
             "cpu_vectors_sampled": cpu_vectors}
+
+
+def measure_solve_calls(torch, dev, reps=4):
+    """Single-call planner.solve() wall time (the per-epoch call Engine._solve
+    makes, engine.py:207-216), as the reference's acceptance check c10 times
+    it (test_acceptance.py:625-632, median <= 30 ms): on the shared scenario
+    table (scenario.build_table of diurnal.yaml, 205 rows, built here through
+    profile_config from the committed prompts) and on the c2 table (44,299 rows)."""
+    import gzip
+    from paper_2509_00642_b200 import profile_config, solve, synth
+    from paper_2509_00642_b200.catalog import default_catalog
+    from paper_2509_00642_b200.profiler import GridProfiler, rows_from_device
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "text.json.gz"), "rt") as fh:
+        doc = json.load(fh)
+    cfg = doc["misc"]["shared2048"]
+    cat = default_catalog()
+    t0 = time.perf_counter()
+    shared = profile_config(cat, doc["corpora"]["shared2048"], seed=cfg["seed"],
+                            noise_sigma=cfg["noise_sigma"], eps_latency=cfg["eps_latency"],
+                            eps_quality=cfg["eps_quality"])
+    profile_s = time.perf_counter() - t0
+    c2 = synth.CONFIGS["c2"]
+    pool, h, noise, scores = synth.records(c2)
+    c2_rows = rows_from_device(GridProfiler(pool, h, scores, device=dev).run(c2.thresholds), pool,
+                               c2.thresholds, lazy=True)
+    out = {"shared_table_profile_config_s": profile_s}
+    for name, rows, catalog in (("shared205", shared.rows, cat),
+                                ("c2_44299", c2_rows, c2.catalog())):
+        solve(rows, catalog, 1.0)                 # device rows built once per table
+        times = []
+        for lam in (0.0, 2.0, 5.0, 11.0, 23.0, 41.0, 61.0, 83.0) * reps:
+            t0 = time.perf_counter()
+            solve(rows, catalog, lam)
+            times.append((time.perf_counter() - t0) * 1e3)
+        times.sort()
+        out[name] = {"rows": len(rows), "calls": len(times),
+                     "median_ms": statistics.median(times),
+                     "p99_ms": times[min(len(times) - 1, int(0.99 * len(times)))]}
+    out["published"] = "PAPER.md:542 ~30 ms MILP per planning cycle; SPEC.md:686 median <= 30 ms"
+    return out
+
+
+def measure_materialise(dt, pool, thresholds):
+    """Host cost of handing the device table to Python: the columnar
+    CascadeRows view (one D2H per column) vs 11M CascadeRow objects."""
+    from paper_2509_00642_b200.profiler import rows_from_device
+    t0 = time.perf_counter()
+    lazy = rows_from_device(dt, pool, thresholds, lazy=True)
+    lazy_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    full = tuple(lazy)
+    full_ms = (time.perf_counter() - t0) * 1e3
+    return {"rows": len(full), "columnar_ms": lazy_ms, "tuple_of_rows_ms": full_ms,
+            "what": "profile_records returns the columnar view (rows built on access)"}
+
+
+def measure_text(torch, dev, n=1_000_000, cpu_prompts=1500):
+    """text -> records (key sort, hardness, keyed noise) for
+    n prompts through text.text_records, next to the reference's per-prompt
+    host cost (oracle port of router.hardness + seeds.stream_normal, sampled)."""
+    import gzip
+    from oracle import text as ot
+    from paper_2509_00642_b200.text import text_records
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "text.json.gz"), "rt") as fh:
+        base = json.load(fh)["corpora"]["c1"]
+    texts = [f"{base[i % len(base)]} {i}" for i in range(n)]
+    text_records(texts[:1000], 0, 0.05)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rec = text_records(texts, 0, 0.05)
+    total_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ot.text_records(texts[:cpu_prompts], 0)
+    cpu_us = (time.perf_counter() - t0) / cpu_prompts * 1e6
+    return {"workload": f"{n} prompts (c1 texts + index), seed 0, sigma 0.05",
+            "prompts": n, "s": total_s, "prompts_per_s": n / total_s,
+            "us_per_prompt": total_s / n * 1e6, "cpu_us_per_prompt": cpu_us,
+            "cpu_kind": "port", "cpu_prompts_sampled": cpu_prompts,
+            "h_mean": float(rec.h.mean())}
 
 
 def _ncu_traffic(name, world, n_light):

@@ -89,7 +89,8 @@ class DeviceRows:
     def __init__(self, rows, catalog, device=None):
         torch = _lib.torch_cuda()
         self.torch = torch
-        self.rows = tuple(rows)
+        from .profiler import CascadeRows
+        self.rows = rows if isinstance(rows, CascadeRows) else tuple(rows)
         self.catalog = catalog
         dev = torch.device(device) if device is not None else torch.device("cuda")
         self.device = dev
@@ -101,12 +102,20 @@ class DeviceRows:
         if not self.rows:
             raise PlannerError("fallback: no serveable rows")
         try:
-            rm = np.array([(index[r.light_id], index[r.heavy_id]) for r in self.rows], dtype=np.int32)
+            if isinstance(self.rows, CascadeRows):      # columnar table: no row objects
+                pair, ids, r_l, r_h, fid = self.rows.columns()
+                pm = np.array([(index[a], index[b]) for a, b in ids], dtype=np.int32)
+                rm = np.ascontiguousarray(pm.reshape(-1, 2)[pair.astype(np.int64)])
+                share = np.ascontiguousarray(np.stack([r_l, r_h], axis=1))
+                fid = np.ascontiguousarray(fid)
+            else:
+                rm = np.array([(index[r.light_id], index[r.heavy_id]) for r in self.rows],
+                              dtype=np.int32)
+                share = np.array([(r.r_light, r.r_heavy) for r in self.rows], dtype=np.float64)
+                fid = np.array([r.fidelity_cost for r in self.rows], dtype=np.float64)
         except KeyError as exc:
             from .catalog import CatalogError
             raise CatalogError(f"unknown-variant: {exc.args[0]!r}") from None
-        share = np.array([(r.r_light, r.r_heavy) for r in self.rows], dtype=np.float64)
-        fid = np.array([r.fidelity_cost for r in self.rows], dtype=np.float64)
         variants = [catalog.by_id(m) for m in ids]
         lat = np.array([[v.latency_s[b] for b in bs] for v in variants], dtype=np.float64)
         mu = np.array([[v.throughput_qps[b] for b in bs] for v in variants], dtype=np.float64)
@@ -244,7 +253,8 @@ def device_rows(rows, catalog) -> DeviceRows:
     """Cached DeviceRows for a (rows, catalog) pair (rebuilt when either changes)."""
     key = (id(rows), id(catalog))
     hit = _CACHE.get(key)
-    if hit is not None and hit.rows == tuple(rows) and hit.catalog is catalog:
+    if hit is not None and hit.catalog is catalog and \
+            (hit.rows is rows or hit.rows == tuple(rows)):
         return hit
     if len(_CACHE) > 32:
         _CACHE.clear()

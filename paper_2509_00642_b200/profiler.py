@@ -32,6 +32,7 @@ from __future__ import annotations
 import hashlib
 import json
 import math
+from collections.abc import Sequence
 from dataclasses import asdict, dataclass
 
 import numpy as np
@@ -657,21 +658,88 @@ class TablePipeline:
         return done
 
 
-def rows_from_device(dt: DeviceTable, pool, thresholds) -> tuple:
-    """Materialise CascadeRow objects (host) from a DeviceTable."""
-    thr = tuple(float(t) for t in thresholds)
-    pair = dt.pair.cpu().numpy()
-    th = dt.theta_pos.cpu().numpy()
-    ta = dt.tau_pos.cpu().numpy()
-    rl = dt.r_light.cpu().numpy().tolist()
-    rh = dt.r_heavy.cpu().numpy().tolist()
-    fid = dt.fid.cpu().numpy().tolist()
-    lat = dt.lat.cpu().numpy().tolist()
+class CascadeRows(Sequence):
+    """The rows of a profiled table, kept columnar (numpy) and turned into
+    ``CascadeRow`` objects only when accessed -- an 11M-row c4 table costs one
+    D2H copy instead of 11M Python objects.  Behaves as the reference's
+    ``tuple[CascadeRow, ...]`` (profiler.py:92-98): len, indexing, slicing,
+    iteration, equality with any sequence of rows, hashing; a row fetched
+    twice is the same object (plans refer to table rows by identity)."""
+
+    def __init__(self, ids, pair, theta_pos, tau_pos, r_light, r_heavy, fid, lat, thresholds):
+        self._ids = list(ids)               # (light_id, heavy_id) per pair id
+        self._cols = (np.asarray(pair), np.asarray(theta_pos), np.asarray(tau_pos),
+                      np.asarray(r_light, dtype=np.float64),
+                      np.asarray(r_heavy, dtype=np.float64),
+                      np.asarray(fid, dtype=np.float64), np.asarray(lat, dtype=np.float64))
+        self._thr = tuple(float(t) for t in thresholds)
+        self._cache = {}
+
+    def __len__(self):
+        return int(self._cols[0].shape[0])
+
+    def _row(self, i):
+        row = self._cache.get(i)
+        if row is None:
+            p, a, b, x1, x2, f, m = (c[i] for c in self._cols)
+            lid, hid = self._ids[int(p)]
+            row = self._cache[i] = CascadeRow(
+                light_id=lid, heavy_id=hid, theta=self._thr[int(a)], tau=self._thr[int(b)],
+                r_light=float(x1), r_heavy=float(x2), fidelity_cost=float(f),
+                mean_latency_s=float(m))
+        return row
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return tuple(self._row(j) for j in range(*i.indices(len(self))))
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("row index out of range")
+        return self._row(i)
+
+    def __iter__(self):
+        n = len(self)
+        step = 1 << 16
+        for s0 in range(0, n, step):
+            chunk = [c[s0:s0 + step].tolist() for c in self._cols]
+            for j, (p, a, b, x1, x2, f, m) in enumerate(zip(*chunk)):
+                row = self._cache.get(s0 + j)
+                if row is None:
+                    lid, hid = self._ids[p]
+                    row = CascadeRow(light_id=lid, heavy_id=hid, theta=self._thr[a],
+                                     tau=self._thr[b], r_light=x1, r_heavy=x2,
+                                     fidelity_cost=f, mean_latency_s=m)
+                yield row
+
+    def columns(self):
+        """(pair ids, (light_id, heavy_id) per pair id, r_light, r_heavy, fid) as arrays."""
+        return self._cols[0], self._ids, self._cols[3], self._cols[4], self._cols[5]
+
+    def __eq__(self, other):
+        if isinstance(other, CascadeRows):
+            return (self._ids == other._ids and self._thr == other._thr and
+                    all(np.array_equal(a, b) for a, b in zip(self._cols, other._cols)))
+        if isinstance(other, (tuple, list, Sequence)) and not isinstance(other, str):
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __hash__(self):
+        return hash(tuple(self))
+
+    def __repr__(self):
+        return f"CascadeRows({len(self)} rows)"
+
+
+def rows_from_device(dt: DeviceTable, pool, thresholds, lazy=False):
+    """Table rows (host) from a DeviceTable: a tuple of CascadeRow objects, or
+    the columnar CascadeRows view (``lazy=True``, one D2H copy per column)."""
+    cols = [getattr(dt, f).cpu().numpy() for f in ("pair", "theta_pos", "tau_pos", "r_light",
+                                                    "r_heavy", "fid", "lat")]
     ids = [(pool[i].id, pool[j].id) for i, j in dt.pairs]
-    return tuple(CascadeRow(light_id=ids[p][0], heavy_id=ids[p][1], theta=thr[a], tau=thr[b],
-                            r_light=x1, r_heavy=x2, fidelity_cost=f, mean_latency_s=m)
-                 for p, a, b, x1, x2, f, m in zip(pair.tolist(), th.tolist(), ta.tolist(), rl, rh,
-                                                  fid, lat))
+    rows = CascadeRows(ids, *cols, thresholds)
+    return rows if lazy else tuple(rows)
 
 
 def _pool_of(pool_or_catalog, eps_latency, eps_quality):
@@ -685,7 +753,8 @@ def _pool_of(pool_or_catalog, eps_latency, eps_quality):
 
 
 def profile_records(pool_or_catalog, h, scores=None, noise=None, thresholds=THRESHOLD_GRID,
-                    eps_latency=0.1, eps_quality=0.1, exact_fid=False, provenance=None):
+                    eps_latency=0.1, eps_quality=0.1, exact_fid=False, provenance=None,
+                    lazy=True):
     """CascadeTable from per-query records (array-level profile_config).
 
     ``h``: hardness in [0, 1] per query; ``scores``: dict model id -> float64[N]
@@ -693,7 +762,8 @@ def profile_records(pool_or_catalog, h, scores=None, noise=None, thresholds=THRE
     scores exactly as profiler.py:134-137.  Records must be in the order the
     reference would use (``stable_text_key`` order of the prompts) for
     ``exact_fid`` to be bitwise-identical; counts, latencies and membership do
-    not depend on order."""
+    not depend on order.  ``lazy`` (default) keeps the rows columnar
+    (``CascadeRows``: a tuple-like view materialising rows on access)."""
     pool = _pool_of(pool_or_catalog, eps_latency, eps_quality)
     h = np.asarray(h, dtype=np.float64) if not hasattr(h, "is_cuda") else h
     if h.shape[0] == 0:
@@ -706,7 +776,7 @@ def profile_records(pool_or_catalog, h, scores=None, noise=None, thresholds=THRE
         scores = np.stack([np.asarray(scores[v.id], dtype=np.float64) for v in pool[:-1]])
     prof = GridProfiler(pool, h, scores)
     dt = prof.run(thresholds, exact_fid=exact_fid)
-    rows = rows_from_device(dt, pool, thresholds)
+    rows = rows_from_device(dt, pool, thresholds, lazy=lazy)
     if provenance is None:
         cat = pool_or_catalog if hasattr(pool_or_catalog, "variants") else None
         provenance = TableProvenance(

@@ -141,6 +141,15 @@ def main():
     tables["edge_random_alt"] = table_doc(rprof.profile_config(
         cat, edge + rand, seed=-8, noise_sigma=0.2, weights=ALT_WEIGHTS,
         thresholds=(0.0, 0.3, 0.3, 0.9, 0.1)))
+    # test_acceptance.py's shared table (scenario.build_table of diurnal.yaml:
+    # gen_prompts(2048, 5), seed 5, default grid) -- the c10 solve-latency table
+    from cascadesim.scenario import build_table, load_scenario
+    sc = load_scenario(os.path.join(REF, "cascadesim", "data", "scenarios", "diurnal.yaml"))
+    corpora["shared2048"] = gen_prompts(sc.profile.n_prompts, sc.seed, sc.profile.hardness_range)
+    shared = build_table(sc, cat)
+    tables["shared2048"] = table_doc(shared)
+    misc_shared = {"seed": sc.seed, "noise_sigma": sc.profile.noise_sigma,
+                   "eps_latency": sc.profile.eps_latency, "eps_quality": sc.profile.eps_quality}
     conf = rprof.profile_config(cat, corpora["conftest160"], seed=42)
     with tempfile.TemporaryDirectory() as tmp:
         path = os.path.join(tmp, "t.json")
@@ -165,7 +174,7 @@ def main():
             "alt_weights": list(ALT_WEIGHTS),
             "noise_keys": [[seed, s] for seed, s in NOISE_KEYS],
             "save_table_conftest160": saved, "load_errors": errors,
-            "catalog_hash_default": cat.content_hash()}
+            "catalog_hash_default": cat.content_hash(), "shared2048": misc_shared}
     doc = {"corpora": corpora, "cases": cases, "tables": tables, "misc": misc}
     with gzip.open(os.path.join(HERE, "text.json.gz"), "wt", encoding="utf-8") as fh:
         json.dump(doc, fh, sort_keys=True)

@@ -50,10 +50,7 @@ def test_pairs_light_to_heavy():
     assert pair_list(list("abcd")) == [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 
 
-def test_prompts_hash_is_reference_hash():
-    # values produced by cascadesim.profiler.prompts_hash / seeds.stable_text_key
-    from tests.goldens import load_json
+def test_prompts_hash_is_order_free():
+    # reference values are checked in test_table_cpu.py / test_text_cpu.py
     assert prompts_hash(["x", "y", "z"]) == prompts_hash(["z", "x", "y"])
-    assert stable_text_key("a cat") == 2998634436011244209 or stable_text_key("a cat") > 0
-    doc = load_json("c1")
-    assert len(doc["prompts_hash"]) == 16
+    assert 0 <= stable_text_key("a cat") < 2 ** 63
