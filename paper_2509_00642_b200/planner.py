@@ -80,6 +80,32 @@ def update_estimate(estimate: float, observed: float, weight: float = EWMA_WEIGH
     return weight * observed + (1.0 - weight) * estimate
 
 
+def row_arrays(rows, index):
+    """Planner inputs of a row sequence: (light, heavy) catalog indices
+    int32[R][2], shares float64[R][2] (r_light, r_heavy) and fidelity
+    float64[R].  A columnar ``CascadeRows`` table is converted column-wise
+    (no row objects); unknown model ids raise CatalogError as the reference
+    catalog lookup does."""
+    from .profiler import CascadeRows
+    try:
+        if isinstance(rows, CascadeRows):
+            pair, pair_ids, r_l, r_h, fid = rows.columns()
+            pm = np.array([(index[a], index[b]) for a, b in pair_ids], dtype=np.int32)
+            rm = np.ascontiguousarray(pm.reshape(-1, 2)[pair.astype(np.int64)])
+            share = np.ascontiguousarray(np.stack([r_l, r_h], axis=1))
+            fid = np.ascontiguousarray(fid)
+        else:
+            rm = np.array([(index[r.light_id], index[r.heavy_id]) for r in rows],
+                          dtype=np.int32).reshape(-1, 2)
+            share = np.array([(r.r_light, r.r_heavy) for r in rows],
+                             dtype=np.float64).reshape(-1, 2)
+            fid = np.array([r.fidelity_cost for r in rows], dtype=np.float64)
+    except KeyError as exc:
+        from .catalog import CatalogError
+        raise CatalogError(f"unknown-variant: {exc.args[0]!r}") from None
+    return rm, share, fid
+
+
 class DeviceRows:
     """A table's rows and its catalog's latency/throughput tables in HBM.
 
@@ -96,26 +122,11 @@ class DeviceRows:
         self.device = dev
         ids = [v.id for v in catalog.variants]
         self.model_ids = ids
-        index = {m: i for i, m in enumerate(ids)}
         bs = tuple(catalog.batch_sizes)
         self.batch_sizes = bs
         if not self.rows:
             raise PlannerError("fallback: no serveable rows")
-        try:
-            if isinstance(self.rows, CascadeRows):      # columnar table: no row objects
-                pair, ids, r_l, r_h, fid = self.rows.columns()
-                pm = np.array([(index[a], index[b]) for a, b in ids], dtype=np.int32)
-                rm = np.ascontiguousarray(pm.reshape(-1, 2)[pair.astype(np.int64)])
-                share = np.ascontiguousarray(np.stack([r_l, r_h], axis=1))
-                fid = np.ascontiguousarray(fid)
-            else:
-                rm = np.array([(index[r.light_id], index[r.heavy_id]) for r in self.rows],
-                              dtype=np.int32)
-                share = np.array([(r.r_light, r.r_heavy) for r in self.rows], dtype=np.float64)
-                fid = np.array([r.fidelity_cost for r in self.rows], dtype=np.float64)
-        except KeyError as exc:
-            from .catalog import CatalogError
-            raise CatalogError(f"unknown-variant: {exc.args[0]!r}") from None
+        rm, share, fid = row_arrays(self.rows, {m: i for i, m in enumerate(ids)})
         variants = [catalog.by_id(m) for m in ids]
         lat = np.array([[v.latency_s[b] for b in bs] for v in variants], dtype=np.float64)
         mu = np.array([[v.throughput_qps[b] for b in bs] for v in variants], dtype=np.float64)

@@ -103,3 +103,29 @@ def test_columnar_rows_behave_as_the_row_tuple(tmp_path):
     t = CascadeTable(rows=rows, provenance=prov)
     assert t.pairs() == [("a", "b"), ("a", "c"), ("b", "c")]
     assert t.rows_for_pair("a", "c") == [r for r in want if r.heavy_id == "c" and r.light_id == "a"]
+
+
+def test_planner_row_arrays_columnar_equals_tuple(tmp_path, gold):
+    """The planner's host conversion gives the same arrays for a columnar
+    CascadeRows table and for the tuple of its rows (catalog indices, not the
+    per-pair id list, feed the device rows)."""
+    from paper_2509_00642_b200.catalog import CatalogError
+    from paper_2509_00642_b200.planner import row_arrays
+    table = load_table(_write(tmp_path, gold["misc"]["save_table_conftest160"]),
+                       catalog=default_catalog())
+    rows = table.rows
+    pairs = sorted({(r.light_id, r.heavy_id) for r in rows})
+    pid = {p: i for i, p in enumerate(pairs)}
+    thr = sorted({r.theta for r in rows} | {r.tau for r in rows})
+    tpos = {t: i for i, t in enumerate(thr)}
+    cols = CascadeRows(pairs, [pid[(r.light_id, r.heavy_id)] for r in rows],
+                       [tpos[r.theta] for r in rows], [tpos[r.tau] for r in rows],
+                       [r.r_light for r in rows], [r.r_heavy for r in rows],
+                       [r.fidelity_cost for r in rows], [r.mean_latency_s for r in rows], thr)
+    assert cols == rows
+    index = {v.id: i for i, v in enumerate(default_catalog().variants)}
+    a, b = row_arrays(cols, index), row_arrays(rows, index)
+    for x, y in zip(a, b):
+        assert x.dtype == y.dtype and np.array_equal(x, y)
+    with pytest.raises(CatalogError, match="unknown-variant"):
+        row_arrays(cols, {k: v for k, v in index.items() if k != pairs[0][0]})
