@@ -14,6 +14,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhadis_b200.so")
+if os.environ.get("HADIS_LIB_VARIANT"):      # A/B builds of the same library (tools/ only)
+    LIB_PATH = os.path.join(_HERE, f"libhadis_b200_{os.environ['HADIS_LIB_VARIANT']}.so")
 
 _c_int, _c_i32, _c_i64, _c_sz, _c_dbl, _c_vp = (ctypes.c_int, ctypes.c_int32, ctypes.c_int64,
                                                ctypes.c_size_t, ctypes.c_double, ctypes.c_void_p)

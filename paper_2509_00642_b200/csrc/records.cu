@@ -43,6 +43,36 @@ constexpr int kBkTile = 8192;         // records per scatter tile   L2 bulk pref
 constexpr int kBkPer = kBkTile / kBkThreads;   // records per thread per tile (even)
 constexpr int kCountThreads = 512;
 
+// B3 (TMA path) geometry: 15 consumer warps + 1 producer warp (512 threads:
+// 128 registers for 16 records per consumer), 7680-record tiles (~7.5
+// records per row and tile at U = 1024: the write-out's row runs, and so its
+// sector efficiency, grow with the tile), ring slots of 8 records per
+// consumer (two per array tile).  Measured at c4 (us): 31 warps x 4 records
+// 369, x 8 363; 15 x 16 359; 2-3 CTAs per SM with proportionally smaller
+// tiles 465-576 (per-tile row costs); 4 ring slots or L2 bulk prefetch: no gain.
+#ifndef HADIS_TMA_CWARPS
+#define HADIS_TMA_CWARPS 15
+#endif
+#ifndef HADIS_TMA_PER
+#define HADIS_TMA_PER 16
+#endif
+#ifndef HADIS_TMA_CHUNK_PER
+#define HADIS_TMA_CHUNK_PER 8
+#endif
+#ifndef HADIS_TMA_SLOTS
+#define HADIS_TMA_SLOTS 3
+#endif
+constexpr int kTmaConsumers = 32 * HADIS_TMA_CWARPS;
+constexpr int kTmaThreads = kTmaConsumers + 32;        // + the producer warp
+constexpr int kTmaPer = HADIS_TMA_PER;                 // records per consumer per tile
+constexpr int kTmaChunkPer = HADIS_TMA_CHUNK_PER;      // records per consumer per ring slot (even)
+constexpr int kTmaChunks = kTmaPer / kTmaChunkPer;     // ring slots per array tile
+constexpr int kTmaChunk = kTmaChunkPer * kTmaConsumers;   // records per ring slot
+constexpr int kTmaTile = kTmaPer * kTmaConsumers;      // records per tile (max)
+constexpr int kTmaSlots = HADIS_TMA_SLOTS;
+constexpr int kTmaBar = 1;                             // named barrier id (consumers)
+static_assert(kTmaPer % kTmaChunkPer == 0 && kTmaChunkPer % 2 == 0, "pairs per chunk");
+
 // Row plan (the `row_plan` buffer shared by B0..B3 and K1), offsets in bytes.
 struct RowPlan {
   uint32_t* row_cnt;     // [kMaxBins]     B1 counts
@@ -491,47 +521,38 @@ bucket_scatter_kernel(const double* __restrict__ h, const double* __restrict__ s
   }
 }
 
-// B3 (TMA-fed): the same scatter with the record arrays streamed into a
-// shared-memory ring by the bulk-copy engine instead of register prefetch.
-// One producer warp (one elected lane) issues cp.async.bulk copies of
-// kTmaChunk-record chunks -- h, then each light model's scores, tile by tile
-// -- into kTmaSlots ring slots, each completing on its "full" mbarrier; the
-// kTmaConsumers consumer threads (16 warps) wait on it, bin the chunk from
-// shared memory and release the slot with one arrive per warp on its "empty"
-// mbarrier.  Loads therefore stay in flight through the tile prologue
-// (ranks, block scan, cursor reservations) and every write-out, and no
-// record data is held in registers across phases.  Consumer-only phases
-// synchronise with a named barrier; the producer never joins them.
-#ifndef HADIS_TMA_CONSUMER_WARPS
-#define HADIS_TMA_CONSUMER_WARPS 31
-#endif
-#ifndef HADIS_TMA_PER_CHUNK
-#define HADIS_TMA_PER_CHUNK 4
-#endif
-#ifndef HADIS_TMA_SLOTS
-#define HADIS_TMA_SLOTS 3
-#endif
-constexpr int kTmaConsumers = 32 * HADIS_TMA_CONSUMER_WARPS;   // consumer threads
-constexpr int kTmaThreads = kTmaConsumers + 32;        // + the producer warp
-#ifndef HADIS_TMA_PER
-#define HADIS_TMA_PER 8
-#endif
-constexpr int kTmaPer = HADIS_TMA_PER;                 // records per consumer per tile
-constexpr int kTmaPerChunk = HADIS_TMA_PER_CHUNK;      // records per consumer per ring chunk
-constexpr int kTmaChunks = kTmaPer / kTmaPerChunk;     // chunks per record array and tile
-constexpr int kTmaChunk = kTmaPerChunk * kTmaConsumers;   // records per ring slot
-constexpr int kTmaTile = kTmaPer * kTmaConsumers;      // records per tile
-constexpr int kTmaSlots = HADIS_TMA_SLOTS;
-constexpr int kTmaBar = 1;                             // named barrier id (consumers)
-
+// B3 (TMA-fed): the scatter with the record arrays streamed into a
+// shared-memory ring by the bulk-copy engine.  One producer warp (one elected
+// lane) issues cp.async.bulk copies of kTmaChunk-record chunks -- h, then each
+// light model's scores, tile by tile -- into kTmaSlots ring slots, each
+// completing on its "full" mbarrier; the 31 consumer warps wait on it, bin the
+// chunk from shared memory and release the slot with one arrive per warp on
+// its "empty" mbarrier, so loads stay in flight through every consumer-only
+// phase.  Each CTA owns one contiguous record range (equal even-sized tiles).
+// Per tile (<= kTmaTile records, kTmaPer per consumer):
+//   H  theta-row bins + shared-memory ranks (ATOMS), hfix kept in registers
+//   S  local row offsets (consumer scan) + one global cursor reservation per
+//      non-empty row (all CTAs append at the same per-row cursor, so the
+//      write frontier of the whole grid stays one dense run per row;
+//      per-CTA precomputed row segments measured 2x slower: ~758K partial
+//      lines alive in L2 instead of ~5K)
+//   P  sorted slot -> global position + tile index; hfix staged in row order
+//      and written out (consecutive threads, consecutive addresses)
+//   Q  per model quad: every consumer bins its own records of the four
+//      models into one 8-byte tau-bin word per record in registers, stores
+//      them at their tile indices (16-byte, conflict-free) and the quad is
+//      written out in sorted order.
+// Uniform grids (the common case) bin with the branch-free uniform_bin_fast;
+// measured (c4): the stores, not the loads, bound this kernel (streaming the
+// records alone runs at 7.0 TB/s; all work without the stores at 5.5 TB/s).
 struct TmaSmem {
   double* ring;               // [kTmaSlots][kTmaChunk]
-  unsigned long long* st64;   // [kTmaTile] hfix staged in row order
-  ushort4* st4;               // [kTmaTile] tau-bins of a model quad per slot (aliases st64)
-  uint32_t* gpos;             // [kTmaTile]
-  uint32_t* cnt;              // [kMaxBins]
-  uint32_t* gbase;            // [kMaxBins]
-  double* thr;                // [U + 2]
+  unsigned long long* st;     // [kTmaTile] hfix in row order, then one quad (tile order)
+  uint32_t* gpos;             // [kTmaTile] sorted slot -> global position
+  uint16_t* sidx;             // [kTmaTile] sorted slot -> tile index
+  uint32_t* co;               // [B1] tile row counts, then local row offsets
+  uint32_t* gb;               // [B1] global base of the tile's run in each row
+  double* thr;                // [U + 2], +inf padded
 };
 
 __device__ __forceinline__ int64_t consumer_excl_scan(int64_t v, int64_t* s_warp, int64_t* total) {
@@ -562,26 +583,239 @@ __device__ __forceinline__ int64_t consumer_excl_scan(int64_t v, int64_t* s_warp
   return excl;
 }
 
+// Uniform-grid bin without a table read, an XU convert or a branch:
+// floor(x (U - 1)) is the low mantissa word of x (U - 1) + 2^52 (rounded
+// toward zero); the answer is floor + 1 away from grid points (|frac - 1/2| <
+// 1/2 - 1e-9, the margin of uniform_bin).  x = 0 and x = 1 (clipped scores)
+// are exact grid points: floor + 1 for #{u <= x}, floor for #{u < x}.
+// ok = false: the caller re-bins with uniform_bin.
+template <bool kLE>
+__device__ __forceinline__ int uniform_bin_fast(double x, double um1, bool* ok) {
+  const double y = __dmul_rn(x, um1);
+  const double t = __dadd_rz(y, 4503599627370496.0);                  // 2^52 + floor(y)
+  const double d = __dadd_rn(y, -__dadd_rn(t, -4503599627370495.5));  // frac(y) - 1/2
+  // x in [0, 1] up to the high word: hi <= 0x3ff00000 admits x in (1, 1 + 2^-20],
+  // where floor(y) = U - 1 still gives the exact answer U (both counts)
+  const uint32_t hi = (uint32_t)__double2hiint(x), lo = (uint32_t)__double2loint(x);
+  const bool edge = (lo == 0u) & ((hi == 0u) | (hi == 0x3ff00000u));   // no short circuits:
+  *ok = (hi <= 0x3ff00000u) & ((fabs(d) < 0.5 - 1e-9) | edge);           // keep it branch-free
+  return __double2loint(t) + (kLE ? 1 : 1 - (int)edge);
+}
+
+// bins of a consumer's records of one ring chunk; kMode 0: uniform grid
+// (fast bins, one warp vote, rare fix-up); 1: guide tables
+template <int kMode, bool kLE>
+__device__ __forceinline__ void bin_chunk(const double* thr, int U, double um1, int mode,
+                                          const uint32_t* guide, const double (&x)[kTmaChunkPer],
+                                          const bool (&valid)[kTmaChunkPer / 2],
+                                          int (&b)[kTmaChunkPer]) {
+  if (kMode == 0) {
+    bool ok = true;
+#pragma unroll
+    for (int e = 0; e < kTmaChunkPer; ++e) {
+      bool oke;
+      b[e] = uniform_bin_fast<kLE>(x[e], um1, &oke);
+      ok &= oke | !valid[e >> 1];
+    }
+    if (__any_sync(0xffffffffu, !ok)) {
+      if (!ok) {
+#pragma unroll
+        for (int e = 0; e < kTmaChunkPer; ++e) b[e] = uniform_bin<kLE>(thr, U, x[e]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kTmaChunkPer; ++e) b[e] = plan_bin<kLE>(mode, thr, U, guide, x[e]);
+  }
+}
+
+// tile index of a consumer's record e (chunk-major, two adjacent records per pair)
+__device__ __forceinline__ int tma_rec(int e, int c) {
+  return (e / kTmaChunkPer) * kTmaChunk + 2 * (((e % kTmaChunkPer) >> 1) * kTmaConsumers + c) +
+         (e & 1);
+}
+
+template <int kMode>
+__device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* full,
+                                                  uint64_t* empty, int64_t* s_warp, int64_t n,
+                                                  int n_light, int U, double hscale,
+                                                  const RowPlan& rp, int64_t r0, int64_t r1,
+                                                  int64_t tile, uint64_t* __restrict__ hfix_rows,
+                                                  uint16_t* __restrict__ bs_rows) {
+  constexpr int kCP = kTmaChunkPer / 2;                // pairs per consumer and chunk
+  const int c = threadIdx.x, lane = c & 31;
+  const int B1 = U + 1;
+  const double um1 = (double)(U - 1);
+  const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  int slot = 0;
+  uint32_t ph = 0;
+  // one ring chunk: the consumer's kTmaChunkPer records (pairs 16-byte loads)
+  auto load_chunk = [&](const bool (&valid)[kCP], double (&x)[kTmaChunkPer]) {
+    mbar_wait_u32(full0 + 8 * slot, ph);
+    const double2* buf = reinterpret_cast<const double2*>(sm.ring + slot * kTmaChunk);
+#pragma unroll
+    for (int p = 0; p < kCP; ++p) {
+      const double2 v = valid[p] ? buf[p * kTmaConsumers + c] : make_double2(0.0, 0.0);
+      x[2 * p] = v.x;
+      x[2 * p + 1] = v.y;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(empty0 + 8 * slot);
+    if (++slot == kTmaSlots) { slot = 0; ph ^= 1u; }
+  };
+  // Pending write-out of the staged array (hfix or the last quad): consumer c
+  // owns sorted slots c + k kTmaConsumers, k < kTmaPer; they are written a
+  // few at a time between ring chunks of the next array, so the loads keep
+  // streaming while the previous array drains.
+  uint2* wo_quad = nullptr;           // null: hfix
+  int wo_tn = 0, wo_done = kTmaPer;
+  auto wo_items = [&](int upto) {
+    for (; wo_done < upto; ++wo_done) {
+      const int i = c + wo_done * kTmaConsumers;
+      if (i < wo_tn) {
+        const uint32_t g = sm.gpos[i];
+        if (wo_quad) wo_quad[g] = reinterpret_cast<const uint2*>(sm.st)[sm.sidx[i]];
+        else hfix_rows[g] = sm.st[i];
+      }
+    }
+  };
+  // rows owned by this consumer (contiguous segment: scan order)
+  const int per = (B1 + kTmaConsumers - 1) / kTmaConsumers;
+  const int i0 = min(B1, c * per), i1 = min(B1, i0 + per);
+  for (int i = i0; i < i1; ++i) sm.co[i] = 0;
+  const int nq = (int)n_quads(n_light);
+  uint2* const orow0 = reinterpret_cast<uint2*>(bs_rows);
+  const int64_t qstride = quad_stride(n);
+  named_sync(kTmaBar, kTmaConsumers);
+  for (int64_t t0 = r0; t0 < r1; t0 += tile) {
+    const int tn = (int)min(tile, r1 - t0);
+    bool valid[kTmaChunks][kCP];                       // tn even: pairs are whole
+#pragma unroll
+    for (int k = 0; k < kTmaChunks; ++k)
+#pragma unroll
+      for (int p = 0; p < kCP; ++p) valid[k][p] = tma_rec(k * kTmaChunkPer + 2 * p, c) < tn;
+    // H: theta-rows and ranks (the previous tile's last quad drains meanwhile)
+    uint32_t key[kTmaPer];
+    uint64_t hf[kTmaPer];
+#pragma unroll
+    for (int k = 0; k < kTmaChunks; ++k) {
+      double x[kTmaChunkPer];
+      int b[kTmaChunkPer];
+      load_chunk(valid[k], x);
+      bin_chunk<kMode, false>(sm.thr, U, um1, mode, rp.guide_lt, x, valid[k], b);
+#pragma unroll
+      for (int j = 0; j < kTmaChunkPer; ++j) {
+        const int e = k * kTmaChunkPer + j;
+        if (valid[k][j >> 1]) {
+          const uint32_t rank = atomicAdd(&sm.co[b[j]], 1u);
+          key[e] = ((uint32_t)b[j] << 16) | rank;
+          hf[e] = (uint64_t)__dmul_rn((x[j] >= 0.0 && x[j] <= 1.0) ? x[j] : 0.0, hscale);
+        } else {
+          key[e] = 0xffffffffu;
+          hf[e] = 0;
+        }
+      }
+      wo_items((k + 1) * kTmaPer / kTmaChunks);
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    // S: local row offsets + one global reservation per non-empty row
+    {
+      int64_t tsum = 0;
+      for (int i = i0; i < i1; ++i) tsum += sm.co[i];
+      int64_t total;
+      uint32_t run = (uint32_t)consumer_excl_scan(tsum, s_warp, &total);
+      for (int i = i0; i < i1; ++i) {
+        const uint32_t cnt = sm.co[i];
+        sm.co[i] = run;
+        sm.gb[i] = cnt ? atomicAdd(&rp.cursor[i], cnt) : 0u;
+        run += cnt;
+      }
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    // P: sorted slots; hfix staged in row order
+#pragma unroll
+    for (int e = 0; e < kTmaPer; ++e) {
+      if (key[e] != 0xffffffffu) {
+        const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
+        const uint32_t s = sm.co[b] + rank;
+        sm.gpos[s] = sm.gb[b] + rank;
+        sm.sidx[s] = (uint16_t)tma_rec(e, c);
+        sm.st[s] = hf[e];
+      }
+    }
+    named_sync(kTmaBar, kTmaConsumers);
+    for (int i = i0; i < i1; ++i) sm.co[i] = 0;       // next tile's counters (offsets read)
+    wo_quad = nullptr;                                 // hfix drains during quad 0
+    wo_tn = tn;
+    wo_done = 0;
+    // Q: model quads, the four models' bins packed in registers
+    for (int q = 0; q < nq; ++q) {
+      uint32_t lo[kTmaPer], hi[kTmaPer];
+      const int nm = min(kQuad, n_light - q * kQuad);
+      const int steps = nm * kTmaChunks;
+#pragma unroll
+      for (int m = 0; m < kQuad; ++m) {
+#pragma unroll
+        for (int k = 0; k < kTmaChunks; ++k) {
+          int b[kTmaChunkPer];
+          if (m < nm) {
+            double x[kTmaChunkPer];
+            load_chunk(valid[k], x);
+            bin_chunk<kMode, true>(sm.thr, U, um1, mode, rp.guide_le, x, valid[k], b);
+            wo_items((m * kTmaChunks + k + 1) * kTmaPer / steps);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kTmaChunkPer; ++j) b[j] = 0;
+          }
+#pragma unroll
+          for (int j = 0; j < kTmaChunkPer; ++j) {
+            const int e = k * kTmaChunkPer + j;
+            if (m == 0) lo[e] = (uint32_t)b[j];
+            else if (m == 1) lo[e] |= (uint32_t)b[j] << 16;
+            else if (m == 2) hi[e] = (uint32_t)b[j];
+            else hi[e] |= (uint32_t)b[j] << 16;
+          }
+        }
+      }
+      wo_items(kTmaPer);
+      named_sync(kTmaBar, kTmaConsumers);              // previous array drained from st
+#pragma unroll
+      for (int e = 0; e < kTmaPer; e += 2)
+        if (valid[e / kTmaChunkPer][(e % kTmaChunkPer) >> 1])
+          *reinterpret_cast<uint4*>(sm.st + tma_rec(e, c)) =
+              make_uint4(lo[e], hi[e], lo[e + 1], hi[e + 1]);
+      named_sync(kTmaBar, kTmaConsumers);
+      wo_quad = orow0 + (int64_t)q * qstride;          // drains during the next quad / tile
+      wo_done = 0;
+    }
+  }
+  wo_items(kTmaPer);
+}
+
 __global__ void __launch_bounds__(kTmaThreads, 1)
 bucket_scatter_tma_kernel(const double* __restrict__ h, const double* __restrict__ scores,
                           int64_t n, int n_light, const double* __restrict__ thr, int U,
                           double hscale, RowPlan rp, uint64_t* __restrict__ hfix_rows,
                           uint16_t* __restrict__ bs_rows) {
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kTmaSlots], empty[kTmaSlots];
   __shared__ int64_t s_warp[32];
-  __shared__ uint32_t s_tile_n;
+  const int B1 = U + 1;
   TmaSmem sm;
   sm.ring = reinterpret_cast<double*>(smem);
-  sm.st64 = reinterpret_cast<unsigned long long*>(sm.ring + kTmaSlots * kTmaChunk);
-  sm.st4 = reinterpret_cast<ushort4*>(sm.st64);
-  sm.gpos = reinterpret_cast<uint32_t*>(sm.st64 + kTmaTile);
-  sm.cnt = sm.gpos + kTmaTile;
-  sm.gbase = sm.cnt + kMaxBins;
-  sm.thr = reinterpret_cast<double*>(sm.gbase + kMaxBins);
-  const int B1 = U + 1;
-  const int64_t chunk = (ceil_div(n, (int64_t)gridDim.x) + 1) & ~(int64_t)1;
-  const int64_t r0 = min(n, (int64_t)blockIdx.x * chunk), r1 = min(n, r0 + chunk);
+  sm.st = reinterpret_cast<unsigned long long*>(sm.ring + kTmaSlots * kTmaChunk);
+  sm.gpos = reinterpret_cast<uint32_t*>(sm.st + kTmaTile);
+  sm.sidx = reinterpret_cast<uint16_t*>(sm.gpos + kTmaTile);
+  sm.co = reinterpret_cast<uint32_t*>(sm.sidx + ((kTmaTile + 1) & ~1));
+  sm.gb = sm.co + B1;
+  sm.thr = reinterpret_cast<double*>(sm.gb + B1 + (((kTmaTile + 1) / 2) & 1));   // 8-byte aligned
+  // one contiguous, even-sized record range per CTA (equal work per SM)
+  const int64_t len = (ceil_div(n, (int64_t)gridDim.x) + 1) & ~(int64_t)1;
+  const int64_t r0 = min(n, (int64_t)blockIdx.x * len), r1 = min(n, r0 + len);
+  // equal even-sized tiles of at most kTmaTile records
+  const int64_t ntiles = ceil_div(r1 - r0, (int64_t)kTmaTile);
+  const int64_t tile = ntiles > 0 ? (ceil_div(r1 - r0, ntiles) + 1) & ~(int64_t)1 : kTmaTile;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTmaSlots; ++i) {
       mbar_init(&full[i], 1);
@@ -598,16 +832,16 @@ bucket_scatter_tma_kernel(const double* __restrict__ h, const double* __restrict
       const uint64_t pol = policy_evict_first();
       int slot = 0;
       uint32_t ph = 0;
-      for (int64_t t0 = r0; t0 < r1; t0 += kTmaTile) {
-        const int64_t tn = min((int64_t)kTmaTile, r1 - t0);
+      for (int64_t t0 = r0; t0 < r1; t0 += tile) {
+        const int64_t tn = min(tile, r1 - t0);
         for (int a = 0; a <= n_light; ++a) {
           const double* src = (a == 0 ? h : scores + (int64_t)(a - 1) * n) + t0;
-          for (int c = 0; c < kTmaChunks; ++c) {
-            const int64_t m = min((int64_t)kTmaChunk, tn - (int64_t)c * kTmaChunk);
+          for (int k = 0; k < kTmaChunks; ++k) {
+            const int64_t m = min((int64_t)kTmaChunk, tn - (int64_t)k * kTmaChunk);
             mbar_wait(&empty[slot], ph ^ 1u);          // slot released by every consumer warp
             if (m > 0) {
               mbar_arrive_expect_tx(&full[slot], (uint32_t)(m * 8));
-              bulk_load(sm.ring + slot * kTmaChunk, src + (int64_t)c * kTmaChunk,
+              bulk_load(sm.ring + (int64_t)slot * kTmaChunk, src + (int64_t)k * kTmaChunk,
                         (uint32_t)(m * 8), &full[slot], pol);
             } else {
               mbar_arrive(&full[slot]);                // empty chunk: complete the phase
@@ -619,131 +853,23 @@ bucket_scatter_tma_kernel(const double* __restrict__ h, const double* __restrict
     }
     return;
   }
-
-  // ---- consumers (threads 0 .. kTmaConsumers-1)
-  const int lane = threadIdx.x & 31;
-  int slot = 0;
-  uint32_t ph = 0;
-  // record e of this consumer: chunk e / kTmaPerChunk, two adjacent records
-  // per 16-byte load
-  auto rec = [](int e) { return 2 * ((e >> 1) * kTmaConsumers + (int)threadIdx.x) + (e & 1); };
-  auto acquire = [&]() { mbar_wait(&full[slot], ph); return sm.ring + slot * kTmaChunk; };
-  auto release = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (++slot == kTmaSlots) { slot = 0; ph ^= 1u; }
-  };
-  // uniform grids (the common case) bin with two compares; others search
-  // with the guide tables (read through L1 from the row plan)
-  const int mode = *rp.nonuniform == 0 ? 0 : (*rp.sparse == 0 ? 1 : 2);
-  auto bin_h = [&](double x) {
-    return mode == 0 ? uniform_bin<false>(sm.thr, U, x)
-                     : plan_bin<false>(mode, sm.thr, U, rp.guide_lt, x);
-  };
-  auto bin_s = [&](double x) {
-    return mode == 0 ? uniform_bin<true>(sm.thr, U, x)
-                     : plan_bin<true>(mode, sm.thr, U, rp.guide_le, x);
-  };
-  for (int64_t t0 = r0; t0 < r1; t0 += kTmaTile) {
-    const int tn = (int)min((int64_t)kTmaTile, r1 - t0);
-    for (int i = threadIdx.x; i < B1; i += kTmaConsumers) sm.cnt[i] = 0;
-    named_sync(kTmaBar, kTmaConsumers);
-    // 1. theta-row + local rank from the two h chunks; hfix kept in registers
-    uint32_t key[kTmaPer];
-    uint64_t hf[kTmaPer];
-#pragma unroll
-    for (int c = 0; c < kTmaChunks; ++c) {
-      const double* buf = acquire();
-      double xs[kTmaPerChunk];                      // 16-byte shared loads, two records each
-#pragma unroll
-      for (int e2 = 0; e2 < kTmaPerChunk; e2 += 2) {
-        const double2 v = reinterpret_cast<const double2*>(buf)[(rec(c * kTmaPerChunk + e2) - c * kTmaChunk) >> 1];
-        xs[e2] = v.x; xs[e2 + 1] = v.y;
-      }
-#pragma unroll
-      for (int e = c * kTmaPerChunk; e < (c + 1) * kTmaPerChunk; ++e) {
-        const int r = rec(e);
-        if (r < tn) {
-          const double x = xs[e - c * kTmaPerChunk];
-          const int b = bin_h(x);
-          const uint32_t rank = atomicAdd(&sm.cnt[b], 1u);
-          key[e] = ((uint32_t)b << 16) | rank;
-          hf[e] = (uint64_t)__dmul_rn((x >= 0.0 && x <= 1.0) ? x : 0.0, hscale);
-        } else {
-          key[e] = 0xffffffffu;
-          hf[e] = 0;
-        }
-      }
-      release();
-    }
-    named_sync(kTmaBar, kTmaConsumers);
-    // 2. local exclusive offsets + one global reservation per non-empty row
-    {
-      const int per = (B1 + kTmaConsumers - 1) / kTmaConsumers;
-      const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
-      int64_t tsum = 0;
-      for (int i = i0; i < i1; ++i) tsum += sm.cnt[i];
-      int64_t total;
-      int64_t run = consumer_excl_scan(tsum, s_warp, &total);
-      for (int i = i0; i < i1; ++i) {
-        const uint32_t c = sm.cnt[i];
-        sm.gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
-        sm.cnt[i] = (uint32_t)run;
-        run += c;
-      }
-      if (threadIdx.x == 0) s_tile_n = (uint32_t)total;
-    }
-    named_sync(kTmaBar, kTmaConsumers);
-    // 3. sorted slot, global position, hfix staged in row order
-#pragma unroll
-    for (int e = 0; e < kTmaPer; ++e) {
-      if (key[e] != 0xffffffffu) {
-        const uint32_t b = key[e] >> 16, rank = key[e] & 0xffffu;
-        const uint32_t s = sm.cnt[b] + rank;
-        sm.gpos[s] = sm.gbase[b] + rank;
-        sm.st64[s] = hf[e];
-        key[e] = s;
-      }
-    }
-    named_sync(kTmaBar, kTmaConsumers);
-    const int cnt = (int)s_tile_n;
-    for (int i = threadIdx.x; i < cnt; i += kTmaConsumers) hfix_rows[sm.gpos[i]] = sm.st64[i];
-    // 4. per light model: two chunks binned into the quad staging, four
-    //    models per write-out (one 8-byte store per record and quad)
-    for (int l = 0; l < n_light; ++l) {
-      const int qm = l % kQuad;
-      if (qm == 0) named_sync(kTmaBar, kTmaConsumers);   // previous write-out done
-      uint16_t* st = reinterpret_cast<uint16_t*>(sm.st4) + qm;    // lane qm of each slot
-#pragma unroll
-      for (int c = 0; c < kTmaChunks; ++c) {
-        const double* buf = acquire();
-        double xs[kTmaPerChunk];
-#pragma unroll
-        for (int e2 = 0; e2 < kTmaPerChunk; e2 += 2) {
-          const double2 v = reinterpret_cast<const double2*>(buf)[(rec(c * kTmaPerChunk + e2) - c * kTmaChunk) >> 1];
-          xs[e2] = v.x; xs[e2 + 1] = v.y;
-        }
-#pragma unroll
-        for (int e = c * kTmaPerChunk; e < (c + 1) * kTmaPerChunk; ++e)
-          if (key[e] != 0xffffffffu)
-            st[4 * key[e]] = (uint16_t)bin_s(xs[e - c * kTmaPerChunk]);
-        release();
-      }
-      if (qm == kQuad - 1 || l == n_light - 1) {
-        named_sync(kTmaBar, kTmaConsumers);
-        ushort4* orow = reinterpret_cast<ushort4*>(bs_rows) + (int64_t)(l / kQuad) * quad_stride(n);
-        // lanes past the last model of a partial quad carry stale bins; K1
-        // reads only the quad's n_light % 4 models
-        for (int i = threadIdx.x; i < cnt; i += kTmaConsumers) orow[sm.gpos[i]] = sm.st4[i];
-      }
-    }
-    named_sync(kTmaBar, kTmaConsumers);
-  }
+  const int mode = *rp.nonuniform == 0 ? 0 : 1;
+  if (mode == 0)
+    scatter_consumers<0>(sm, full, empty, s_warp, n, n_light, U, hscale, rp, r0, r1, tile,
+                         hfix_rows, bs_rows);
+  else
+    scatter_consumers<1>(sm, full, empty, s_warp, n, n_light, U, hscale, rp, r0, r1, tile,
+                         hfix_rows, bs_rows);
 }
 
+// dynamic shared memory limit of the TMA scatter (227 KB minus its static part)
+constexpr size_t kTmaSmemMax = 227 * 1024 - 2 * 8 * kTmaSlots - 8 * 32 - 64;
+
 static size_t scatter_tma_smem(int U) {
-  return (size_t)8 * kTmaSlots * kTmaChunk + (size_t)8 * kTmaTile + (size_t)4 * kTmaTile +
-         (size_t)4 * 2 * kMaxBins + (size_t)8 * (U + 2);
+  const size_t B1 = (size_t)U + 1;
+  const size_t T = kTmaTile, T2 = (T + 1) & ~(size_t)1;
+  return (size_t)8 * kTmaSlots * kTmaChunk + 8 * T + 4 * T + 2 * T2 +
+         4 * (2 * B1 + ((T2 / 2) & 1)) + (size_t)8 * (U + 2);
 }
 
 // K1: one CTA per (row chunk, model quad).  Each record's hfix (8 B) and its
@@ -1012,12 +1138,15 @@ extern "C" int hadis_records_scatter(const double* h, const double* scores, int6
   int64_t sgrid = ceil_div(n, kBkTile);
   if (sgrid > kNumSMs) sgrid = kNumSMs;
   const char* legacy = getenv("HADIS_B3_REGISTER_PATH");   // A/B switch for measurements
-  if (vec && !(legacy && legacy[0] == '1')) {
-    // aligned record arrays: the TMA-fed scatter (binning mode read on the device)
-    const size_t tsmem = scatter_tma_smem(n_unique);
+  const size_t tsmem = scatter_tma_smem(n_unique);
+  if (vec && tsmem <= kTmaSmemMax && !(legacy && legacy[0] == '1')) {
+    // aligned record arrays: the TMA-fed scatter over the plan's record ranges
+    // (binning mode read on the device)
     HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_tma_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
-    bucket_scatter_tma_kernel<<<(unsigned)sgrid, kTmaThreads, tsmem, st>>>(
+    int64_t tgrid = ceil_div(n, kTmaTile);
+    if (tgrid > kNumSMs) tgrid = kNumSMs;
+    bucket_scatter_tma_kernel<<<(unsigned)tgrid, kTmaThreads, tsmem, st>>>(
         h, scores, n, n_light, thr_unique, n_unique, hscale, rp, hfix_rows, bs_rows);
     HADIS_LAUNCH_CHECK();
     hadis_count_launches(1);
