@@ -410,7 +410,7 @@ def run_ours(args, cfg):
                                                                        + ms_k2))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
-                         "kernel": "B3 bucket_scatter_kernel (row-bucketed record store), rank 0",
+                         "kernel": "B3 bucket_scatter_tma_kernel (row-bucketed record store), rank 0",
                          "peak_kind": peak_kind,
                          "algorithmic_bytes": alg_bytes, "bytes_moved_by_design": moved,
                          "moved_gbs": moved / (ms_b * 1e-3) / 1e9 if ms_b > 0 else 0.0},

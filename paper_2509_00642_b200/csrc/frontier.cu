@@ -374,16 +374,23 @@ struct RowSmem {
 __device__ __forceinline__ bool row_task(const Grid& g, const PairConst* __restrict__ pcs,
                                          const int32_t* __restrict__ group_p0,
                                          const int32_t* __restrict__ n_groups, RowSmem& sm,
-                                         int* p0, int* p1, int* k) {
-  const int grp = blockIdx.y;
+                                         int* p0, int* p1, int* k, int kstride = 1,
+                                         int pchunks = 1) {
+  const int grp = blockIdx.y / pchunks;
   if (grp >= *n_groups) return false;
   *p0 = group_p0[grp];
   *p1 = group_p0[grp + 1];
+  if (pchunks > 1) {                               // this CTA's share of the partners
+    const int cs = (*p1 - *p0 + pchunks - 1) / pchunks;
+    *p0 += (blockIdx.y % pchunks) * cs;
+    *p1 = min(*p1, *p0 + cs);
+    if (*p0 >= *p1) return false;
+  }
   const int np = *p1 - *p0;                      // <= kMaxGroup (checked on the host)
   for (int i = threadIdx.x; i < np * (int)(sizeof(PairConst) / 8); i += blockDim.x)
     reinterpret_cast<double*>(sm.pc)[i] = reinterpret_cast<const double*>(pcs + *p0)[i];
   __syncthreads();
-  *k = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  *k = (blockIdx.x * kRowWarps + (threadIdx.x >> 5)) * kstride;
   return *k < g.U && g.row_start[*k];
 }
 
@@ -503,13 +510,22 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 // dominated by an earlier cell of its row, which sits in the same or a lower
 // bucket).  Reads the current minima first (all in flight): most cells do
 // not lower them.
+// Sampled: F1 walks every kstride-th theta-row only.  Every minimum is still
+// a real cell's S, so the prefix minima G' >= G remain valid domination
+// certificates for F3; they are only weaker (c4, measured: stride 4 -> F1
+// 314 -> ~115 us, candidates 12.4M -> 13.9M, step -145 us; strides 2 / 3 /
+// 5 / 6 / 8 / 16 and 1 / 4 / 8 partner chunks per row: slower).  Skipping
+// windows above a sampled snapshot in a second full F1 pass, or whole F3
+// windows above G at their first cell, measured no gain: the row walk
+// itself, not the per-cell bucket work, is F1/F3's cost.
 __global__ void __launch_bounds__(kRowWarps * 32, 32 / kRowWarps)   // 4 CTAs/SM at 8 warps
 bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restrict__ group_p0,
-                  const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin) {
+                  const int32_t* __restrict__ n_groups, unsigned long long* __restrict__ bmin,
+                  int kstride, int pchunks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
   int p0, p1, k;
-  if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k)) return;
+  if (!row_task(g, pcs, group_p0, n_groups, sm, &p0, &p1, &k, kstride, pchunks)) return;
   const int lane = threadIdx.x & 31;
   const double dRk = (double)slot_cnt(g, sm.pc[0].slot)[(int64_t)k * g.B1 + g.U];
   const uint32_t* s_nH = sm.nH[threadIdx.x >> 5];
@@ -1671,7 +1687,19 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
   HADIS_CUDA_TRY(cudaFuncSetAttribute(filter_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-  bucket_min_kernel<<<row_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cmin);
+#ifndef HADIS_F1_STRIDE
+#define HADIS_F1_STRIDE 4      // F1 over every 4th theta-row only
+#endif
+#ifndef HADIS_F1_CHUNKS
+#define HADIS_F1_CHUNKS 2      // partner chunks per row (parallelism of the sampled F1)
+#endif
+  {
+    constexpr int kS = HADIS_F1_STRIDE, kC = HADIS_F1_CHUNKS;
+    const dim3 f1_grid((unsigned)ceil_div(ceil_div(n_unique, kS), kRowWarps),
+                       (unsigned)(n_pairs * kC));
+    bucket_min_kernel<<<f1_grid, kRowWarps * 32, rsm, st>>>(g, pcs, group_p0, n_groups, cmin, kS,
+                                                            kC);
+  }
   auto prefix = [&](const unsigned long long* mins, int nbk, unsigned long long* tm, double* pre) {
     const int tiles = (int)ceil_div(nbk, kPrefTile);
     prefix_tile_min_kernel<<<dim3(tiles, n_pairs), kScanThreads, 0, st>>>(mins, nbk, tm);
