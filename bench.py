@@ -338,13 +338,15 @@ def run_ours(args, cfg):
                                            stage(4, 5))
 
     # ---- e2e: host buffers, H2D + build + D2H of the row arrays every step.
-    # TablePipeline on every rank (double-buffered; set i's H2D overlaps set
-    # i-1's build and set i-2's D2H); with N ranks each streams its own shard.
+    # N = 1: TablePipeline (double-buffered; set i's H2D overlaps set i-1's
+    # build and set i-2's D2H).  N > 1: every step copies the rank's records
+    # in, builds its shard, all-gathers the slabs, merges and copies the whole
+    # merged table out (the merge is inside the e2e step as well).
     h2d = (h_pin.numel() + sc_pin.numel()) * 8 if plan is not None else 0
     d2h = 0
     barrier()
     e2e_steps = max(3, min(args.steps, 8))
-    if plan is not None:
+    if plan is not None and world == 1:
         from paper_2509_00642_b200.profiler import TablePipeline
         pipe = TablePipeline(pool, n, sc_pin.shape[0], thr, pairs=mine, device=dev,
                              score_slots=slots if world > 1 else None)

@@ -354,6 +354,9 @@ struct __align__(16) ListCand {
 // layout keeps staging stores and per-lane reads conflict-free.  Rows that
 // repeat an earlier row's R[k] (same row class) are exact duplicates and are
 // skipped.
+#ifndef HADIS_ROW_FSCAN
+#define HADIS_ROW_FSCAN 1      // float upper-bound row scan (c4: -18 us, same candidates)
+#endif
 constexpr int kRowWarps = 8;         // rows per CTA (4: no gain)
 constexpr int kCoarseShift = 4;      // F1/F3 latency buckets: the fine ones >> 4
                                      // (3 and 5 measured: F1 vs candidate trade-off, no gain)
@@ -399,9 +402,9 @@ __device__ __forceinline__ bool row_task(const Grid& g, const PairConst* __restr
 // minima and compares run on the FP64 pipe, which has the slack -- u64 keys
 // cost four ALU ops per min); bit j of take = the cell passes the row test -- strict
 // prefix-min (F1) or class start within 2 delta of the prefix-min (F3).
-template <bool kFilter, typename F, typename W>
+template <bool kFilter, typename F, typename W, typename P>
 __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0, int p1, int k,
-                                             F&& visit, W&& window_done) {
+                                             F&& visit, W&& window_done, P&& pre) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* C = slot_cnt(g, sm.pc[0].slot);
   const uint64_t* Sh = slot_hs(g, sm.pc[0].slot);
@@ -467,6 +470,18 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         }
         double* const carry = &sm.carry[warp][p - q0];
         const double c0 = lane == 0 ? *carry : INFINITY;
+#if HADIS_ROW_FSCAN
+        // scan of upper bounds in float (rounded up): run / carry may exceed
+        // the exact prefix minima, so the row tests only keep MORE cells
+        float fincl = __double2float_ru(dmin(lmin, c0));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float o = __shfl_up_sync(0xffffffffu, fincl, off);
+          if (lane >= off) fincl = fminf(fincl, o);
+        }
+        double run = (double)__shfl_up_sync(0xffffffffu, fincl, 1);
+        const double tot = (double)__shfl_sync(0xffffffffu, fincl, 31);
+#else
         double incl = dmin(lmin, c0);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -475,6 +490,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         }
         double run = __shfl_up_sync(0xffffffffu, incl, 1);
         const double tot = __shfl_sync(0xffffffffu, incl, 31);
+#endif
         if (lane == 0) {
           run = c0;
           *carry = tot;
@@ -496,6 +512,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
       };
       for (int p = q0; p < q1; ++p) {
         double sv[kRowT];
+        pre(p, sm.pc[p - p0]);                     // loads that need no scan result
         const unsigned take = scan(p, sv);
         visit(p, sm.pc[p - p0], w0, sv, take);
       }
@@ -529,32 +546,34 @@ bucket_min_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __re
   const int lane = threadIdx.x & 31;
   const double dRk = (double)slot_cnt(g, sm.pc[0].slot)[(int64_t)k * g.B1 + g.U];
   const uint32_t* s_nH = sm.nH[threadIdx.x >> 5];
-  row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
+  int bk[kRowT];
+  unsigned long long cur[kRowT];
+  row_traverse<false>(g, sm, p0, p1, k, [&](int p, const PairConst&, int,
                                             const double* sv, unsigned take) {
     unsigned long long* const bp = bmin + (int64_t)p * (g.nbuckets >> kCoarseShift);
-    const double xr = __dmul_rn(dRk, pc.Ll);
-    int bk[kRowT];
-    unsigned long long cur[kRowT];
-#pragma unroll
-    for (int j = 0; j < kRowT; ++j)                // only taken cells need a bucket
-      bk[j] = (take >> j & 1u)
-                  ? bucket_of_x(pc, g.nbuckets,
-                                __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh))) >>
-                        kCoarseShift
-                  : -1 - j;
     // row-frontier keys strictly decrease along the walk: of consecutive taken
     // cells in one coarse bucket only the last can lower its minimum
 #pragma unroll
     for (int j = 0; j + 1 < kRowT; ++j)
       if ((take >> (j + 1) & 1u) && bk[j + 1] == bk[j]) take &= ~(1u << j);
 #pragma unroll
-    for (int j = 0; j < kRowT; ++j) cur[j] = (take >> j & 1u) ? bp[bk[j]] : 0ull;
-#pragma unroll
     for (int j = 0; j < kRowT; ++j) {
       const unsigned long long key = order_key_fast(sv[j]);
       if ((take >> j & 1u) && key < cur[j]) atomicMin(bp + bk[j], key);
     }
-  }, [](int) {});
+  }, [](int) {}, [&](int p, const PairConst& pc) {
+    // every cell's coarse bucket and current minimum, loaded before the row
+    // scan so their latency overlaps it (past the row end: bucket of nH = 0)
+    const unsigned long long* const bp = bmin + (int64_t)p * (g.nbuckets >> kCoarseShift);
+    const double xr = __dmul_rn(dRk, pc.Ll);
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j) {
+      bk[j] = bucket_of_x(pc, g.nbuckets,
+                          __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh))) >>
+              kCoarseShift;
+      cur[j] = bp[bk[j]];
+    }
+  });
 }
 
 // ------------------------------------------------- F2: exclusive prefix minima
@@ -857,19 +876,9 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const double* s_SHs = sm.SHs[warp];
   const double* s_LP = sm.LP[warp];
   int cnt = 0;                                     // this lane's candidates in the window
+  double gv[kRowT];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
                                            const double* sv, unsigned take) {
-    const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
-    const double xr = __dmul_rn(dRk, pc.Ll);
-    int bk[kRowT];
-    double gv[kRowT];
-#pragma unroll
-    for (int j = 0; j < kRowT; ++j)                // only cells passing the row test
-      bk[j] = (take >> j & 1u) ? bucket_of_x(pc, g.nbuckets,
-                                             __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh)))
-                               : 0;
-#pragma unroll
-    for (int j = 0; j < kRowT; ++j) gv[j] = (take >> j & 1u) ? gp[bk[j] >> kCoarseShift] : -INFINITY;
 #pragma unroll
     for (int j = 0; j < kRowT; ++j)
       if (!(sv[j] <= gv[j] + pc.delta2_S)) take &= ~(1u << j);
@@ -915,6 +924,16 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
         ++at;
       }
     }
+  }, [&](int p, const PairConst& pc) {
+    // every cell's bucket prefix minimum, loaded before the row scan so the
+    // latency overlaps it
+    const double* const gp = gpre + (int64_t)p * (g.nbuckets >> kCoarseShift);
+    const double xr = __dmul_rn(dRk, pc.Ll);
+#pragma unroll
+    for (int j = 0; j < kRowT; ++j)
+      gv[j] = gp[bucket_of_x(pc, g.nbuckets,
+                             __dadd_rn(xr, __dmul_rn(u32_to_double(s_nH[j * kRowPad + lane]), pc.Lh))) >>
+                 kCoarseShift];
   });
 }
 

@@ -856,3 +856,30 @@ def test_graph_replay_survives_workspace_reallocation(gpu_device):
     prof.run(tuple(i / 200 for i in range(201)))       # bigger grid: reallocates workspace
     got = _dt_arrays(replay())
     assert all(np.array_equal(want[k], v) for k, v in got.items())
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_line(gpu_device):
+    """bench.py's N > 1 arm under torchrun (2 ranks, gloo, sharing the box's
+    GPU): the timed step (local build + slab all-gather + merge kernel) runs
+    and rank 0 prints one JSON line whose table has the 1-rank row count."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = ["--config", "c2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+            "--no-allocation"]
+    one = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args,
+                         capture_output=True, text=True, timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    env = dict(os.environ, HADIS_DIST_BACKEND="gloo")
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                          "--nproc-per-node", "2", os.path.join(root, "bench.py"), "--gpus", "2"]
+                         + args, capture_output=True, text=True, env=env, timeout=900)
+    assert two.returncode == 0, two.stderr[-3000:]
+    l1 = json.loads([x for x in one.stdout.splitlines() if x.startswith("{")][-1])
+    l2 = json.loads([x for x in two.stdout.splitlines() if x.startswith("{")][-1])
+    assert l2["n_gpus"] == 2 and l2["value"] > 0 and l2["ms_per_step"] > 0
+    assert l2["config"]["rows"] == l1["config"]["rows"]
+    assert "merge" in l2 and l2["merge"]["row_bytes"] == 44
