@@ -26,6 +26,9 @@
 //   F12 emit           kept-cell bitmap -> rows in (theta, tau) order
 //   F13/F14            exact fidelity patch for emitted rows
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cfloat>
 #include <cmath>
 
@@ -369,7 +372,6 @@ struct RowSmem {
   uint32_t nH[kRowWarps][kRowT * kRowPad];  // heavy-served records (u32: 4 CTAs/SM fit)
   double SHs[kRowWarps][kRowT * kRowPad];   // their hardness sum * 2^-shift
   double LP[kRowWarps][kRowT * kRowPad];    // light part of the fid* numerator
-  uint8_t cls[kRowWarps][kRowT * kRowPad];  // 1 = first of its duplicate run, 2 = past the end
   double carry[kRowWarps][kMaxGroup];
   PairConst pc[kMaxGroup];
 };
@@ -417,7 +419,6 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
   uint32_t* s_nH = sm.nH[warp];
   double* s_SHs = sm.SHs[warp];
   double* s_LP = sm.LP[warp];
-  uint8_t* s_cls = sm.cls[warp];
   {
     const int q0 = p0, q1 = p1;
     for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = INFINITY;
@@ -433,6 +434,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         shv[r] = t < g.U ? Sh[rk + t] : 0ull;
       }
       uint32_t prev = w0 > 0 ? C[rk + w0 - 1] : 0u;  // C at the cell before the window
+      uint32_t cls_m[kRowT];                       // bit l of cls_m[r]: cell r*32+l starts its class
 #pragma unroll
       for (int r = 0; r < kRowT; ++r) {
         const int i = r * 32 + lane, t = w0 + i;
@@ -447,14 +449,19 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
           s_nH[at] = nH;
           s_SHs[at] = __dmul_rn((double)SH, inv);
           s_LP[at] = light_part(bl, pl, (double)(n - nH), __dmul_rn((double)(Htot - SH), inv));
-          s_cls[at] = t == 0 || nr != left;
         } else {                                         // past the row end: S = +inf
           s_nH[at] = 0u;
           s_SHs[at] = 0.0;
           s_LP[at] = INFINITY;
-          s_cls[at] = 2;
         }
+        cls_m[r] = __ballot_sync(0xffffffffu, t < g.U && (t == 0 || nrv[r] != left));
       }
+      // this lane's cells are w0 + 4 lane + j: bits 4 (lane % 8) + j of cls_m[lane / 8]
+      const int qr = lane >> 3;
+      const uint32_t cls4 =
+          ((qr == 0 ? cls_m[0] : qr == 1 ? cls_m[1] : qr == 2 ? cls_m[2] : cls_m[3]) >>
+           (4 * (lane & 7))) & 15u;
+      static_assert(kRowT == 4, "class-start bits: 4 cells per lane");
       __syncwarp();
       // one partner: S of the lane's cells, warp scan of the lane minima (the
       // row carry enters through lane 0, so only lane 0 touches it), row test
@@ -501,7 +508,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         for (int j = 0; j < kRowT; ++j) {
           bool t_ok;
           if (kFilter) {
-            t_ok = s_cls[j * kRowPad + lane] == 1 && sv[j] <= run + dpc;
+            t_ok = ((cls4 >> j) & 1u) && sv[j] <= run + dpc;
           } else {
             t_ok = sv[j] < run;
           }
@@ -1007,11 +1014,26 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     const double G = __ddiv_rn(GS, dn);
     const double lo = cd.fid - d2, hi = cd.fid + d2;
     bool kill = G < lo, close = G <= hi && !kill;
-    for (int64_t j = s0; j < s1; ++j) {
-      const double lat_j = grp.c[j].lat, fid_j = grp.c[j].fid;
-      const bool le = lat_j <= cd.lat;
-      kill |= le & (fid_j < lo);
-      close |= le & (fid_j <= hi) & (j != i);
+    {                                                // kU mates' loads in flight per step
+      constexpr int kU = 8;                          // (c4: -12 us vs one at a time)
+      int64_t j = s0;
+      for (; j + kU <= s1; j += kU) {
+        double2 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = *reinterpret_cast<const double2*>(&grp.c[j + u].lat);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const bool le = v[u].x <= cd.lat;
+          kill |= le & (v[u].y < lo);
+          close |= le & (v[u].y <= hi) & (j + u != i);
+        }
+      }
+      for (; j < s1; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(&grp.c[j].lat);
+        const bool le = v.x <= cd.lat;
+        kill |= le & (v.y < lo);
+        close |= le & (v.y <= hi) & (j != i);
+      }
     }
     if (kill) continue;
     if (!close) {
@@ -1736,6 +1758,30 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
     tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
+  if (getenv("HADIS_DEBUG_BUCKETS")) {             // measurement aid: fine-bucket occupancy
+    std::vector<uint32_t> hc(pb);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(hc.data(), bcnt, 4 * pb, cudaMemcpyDeviceToHost);
+    double s1 = 0, s2 = 0;
+    uint32_t mx = 0;
+    int64_t hist[33] = {0}, nz = 0;
+    for (int64_t i = 0; i < pb; ++i) {
+      const uint32_t m = hc[i];
+      if (!m) continue;
+      ++nz;
+      s1 += m;
+      s2 += (double)m * m;
+      mx = m > mx ? m : mx;
+      int lb = 0;
+      while ((1u << (lb + 1)) <= m) ++lb;
+      hist[lb] += m;
+    }
+    fprintf(stderr, "buckets: %lld non-empty of %lld, candidates %.0f, mates/cand %.2f, max %u\n",
+            (long long)nz, (long long)pb, s1, s2 / (s1 > 0 ? s1 : 1), mx);
+    for (int lb = 0; lb < 33; ++lb)
+      if (hist[lb]) fprintf(stderr, "  bucket size [%u, %u): %lld candidates\n", 1u << lb,
+                            lb < 31 ? 2u << lb : 0u, (long long)hist[lb]);
+  }
   // grid sizes of the two grid-stride passes measured at c4 (4 / 32 CTAs per SM)
   group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, lst, counters + 5, cand_cap, nb, (double)n, boff,
                                                   bcur, grp, bmin);
