@@ -370,8 +370,7 @@ constexpr int kRowPad = 33;
 
 struct RowSmem {
   uint32_t nH[kRowWarps][kRowT * kRowPad];  // heavy-served records (u32: 4 CTAs/SM fit)
-  double SHs[kRowWarps][kRowT * kRowPad];   // their hardness sum * 2^-shift
-  double LP[kRowWarps][kRowT * kRowPad];    // light part of the fid* numerator
+  double2 hl[kRowWarps][kRowT * kRowPad];   // (hardness sum * 2^-shift, light part of S)
   double carry[kRowWarps][kMaxGroup];
   PairConst pc[kMaxGroup];
 };
@@ -417,8 +416,7 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
   const uint64_t Hnb = Htot - Sh[rk + g.U];        // hardness of bypassed records
   const double bl = sm.pc[0].bl, pl = sm.pc[0].pl, inv = g.inv_scale;
   uint32_t* s_nH = sm.nH[warp];
-  double* s_SHs = sm.SHs[warp];
-  double* s_LP = sm.LP[warp];
+  double2* s_hl = sm.hl[warp];
   {
     const int q0 = p0, q1 = p1;
     for (int p = q0 + lane; p < q1; p += 32) sm.carry[warp][p - q0] = INFINITY;
@@ -447,12 +445,12 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
           const uint64_t SH = Hnb + shv[r];
           const uint32_t nH = (n - Rk) + nr;
           s_nH[at] = nH;
-          s_SHs[at] = __dmul_rn((double)SH, inv);
-          s_LP[at] = light_part(bl, pl, (double)(n - nH), __dmul_rn((double)(Htot - SH), inv));
+          s_hl[at] = make_double2(__dmul_rn((double)SH, inv),
+                                  light_part(bl, pl, (double)(n - nH),
+                                             __dmul_rn((double)(Htot - SH), inv)));
         } else {                                         // past the row end: S = +inf
           s_nH[at] = 0u;
-          s_SHs[at] = 0.0;
-          s_LP[at] = INFINITY;
+          s_hl[at] = make_double2(0.0, INFINITY);
         }
         cls_m[r] = __ballot_sync(0xffffffffu, t < g.U && (t == 0 || nrv[r] != left));
       }
@@ -472,7 +470,8 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
 #pragma unroll
         for (int j = 0; j < kRowT; ++j) {
           const int at = j * kRowPad + lane;
-          sv[j] = fid_num(bh, ph, u32_to_double(s_nH[at]), s_SHs[at], s_LP[at]);
+          const double2 v = s_hl[at];
+          sv[j] = fid_num(bh, ph, u32_to_double(s_nH[at]), v.x, v.y);
           lmin = dmin(lmin, sv[j]);
         }
         double* const carry = &sm.carry[warp][p - q0];
@@ -880,8 +879,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
   const bool sorted_thr = *g.sorted != 0;          // first_pos increasing: rep = own rank
   const double dRk = (double)C[(int64_t)k * g.B1 + g.U];
   const uint32_t* s_nH = sm.nH[warp];
-  const double* s_SHs = sm.SHs[warp];
-  const double* s_LP = sm.LP[warp];
+  const double2* s_hl = sm.hl[warp];
   int cnt = 0;                                     // this lane's candidates in the window
   double gv[kRowT];
   row_traverse<true>(g, sm, p0, p1, k, [&](int p, const PairConst& pc, int,
@@ -926,7 +924,7 @@ filter_kernel(Grid g, const PairConst* __restrict__ pcs, const int32_t* __restri
           const int t = w0 + lane * kRowT + j;
           lst[at] = ListCand{(uint32_t)p,
                              krep + (uint32_t)(sorted_thr ? t : rep_tau(g, C, k, t, true)),
-                             fid_num(pc.bh, pc.ph, dnH, s_SHs[a], s_LP[a])};
+                             fid_num(pc.bh, pc.ph, dnH, s_hl[a].x, s_hl[a].y)};
         }
         ++at;
       }
