@@ -63,7 +63,20 @@ struct Grid {
   const int32_t* row_rep;   // rank with the smallest first_pos in k's row class
   const uint8_t* row_start; // 1 if k starts its row class (R[k-1] < R[k])
   const int32_t* sorted;    // *sorted != 0: first_pos increases with rank (sorted list)
+  double rn;                // RN(1 / n): divisions by n through div_n
 };
+
+// a / n correctly rounded, for the fixed divisor n (record count, < 2^32) and
+// rn = RN(1/n): q0 = RN(a rn) is within one ulp of a/n, the residual a - n q0
+// is exact with one FMA, and RN(q0 + r rn) is then the correctly rounded
+// quotient (Markstein's theorem; no over/underflow for |a| < 2^64) -- three
+// FP64 ops instead of __ddiv_rn's reciprocal refinement and slow-path checks.
+// Checked against IEEE division on 6e8 random and near-midpoint cases (n up to
+// 2^33) and by every bit-exact table test.
+__device__ __forceinline__ double div_n(double a, double dn, double rn) {
+  const double q0 = __dmul_rn(a, rn);
+  return __fma_rn(__fma_rn(-q0, dn, a), rn, q0);
+}
 
 struct CellVal {
   double lat, fid;
@@ -107,9 +120,9 @@ __device__ __forceinline__ CellVal eval_cell(const Grid& g, const PairConst& pc,
   v.n_keep_light = Rk;
   v.n_heavy = nH;
   const double dn = (double)g.n;
-  v.lat = __ddiv_rn(__dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh)), dn);
+  v.lat = div_n(__dadd_rn(__dmul_rn((double)Rk, pc.Ll), __dmul_rn((double)nH, pc.Lh)), dn, g.rn);
   const double lp = light_part(pc.bl, pc.pl, (double)(n - nH), __dmul_rn((double)SL, g.inv_scale));
-  v.fid = __ddiv_rn(fid_num(pc.bh, pc.ph, (double)nH, __dmul_rn((double)SH, g.inv_scale), lp), dn);
+  v.fid = div_n(fid_num(pc.bh, pc.ph, (double)nH, __dmul_rn((double)SH, g.inv_scale), lp), dn, g.rn);
   return v;
 }
 
@@ -806,7 +819,7 @@ __device__ void decide_one(const Grid& g, const PairConst& pc, int p, uint32_t c
   const int64_t idx = grid_index(g, k, t);
   bool killed = false, unsure = false;
   // fl(S / n) is exactly the lower buckets' min fid*
-  const double G = __ddiv_rn(G_S, (double)g.n);
+  const double G = div_n(G_S, (double)g.n, g.rn);
   if (G < fid - pc.delta2) {
     killed = true;
   } else if (G <= fid + pc.delta2) {
@@ -969,8 +982,8 @@ __global__ void group_cands_kernel(Grid g, const PairConst* __restrict__ pcs,
     // beaten by a candidate at lower-or-equal latency, so the exclusive
     // prefix of these minima is the exact fine G
     atomicMin(&fmin[key], (unsigned long long)order_key(cd.fid));
-    cd.lat = __ddiv_rn(cd.lat, dn);       // the list holds raw numerators
-    cd.fid = __ddiv_rn(cd.fid, dn);
+    cd.lat = div_n(cd.lat, dn, g.rn);     // the list holds raw numerators
+    cd.fid = div_n(cd.fid, dn, g.rn);
     grp.c[(int64_t)boff[key] + atomicAdd(&bcur[key], 1u)] = cd;
   }
 }
@@ -1009,7 +1022,7 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     const int64_t s1 = min((int64_t)boff[key + 1], m);   // exclusive scan: next start
     const double GS = gpre[key];
     const double d2 = pcs[p].delta2;
-    const double G = __ddiv_rn(GS, dn);
+    const double G = div_n(GS, dn, g.rn);
     const double lo = cd.fid - d2, hi = cd.fid + d2;
     bool kill = G < lo, close = G <= hi && !kill;
     {                                                // kU mates' loads in flight per step
@@ -1504,8 +1517,8 @@ emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __re
     out.pair[r] = p;
     out.theta_pos[r] = g.first_pos[k];
     out.tau_pos[r] = g.first_pos[t];
-    out.r_light[r] = __ddiv_rn((double)v.n_keep_light, dn);
-    out.r_heavy[r] = __ddiv_rn((double)v.n_heavy, dn);
+    out.r_light[r] = div_n((double)v.n_keep_light, dn, g.rn);
+    out.r_heavy[r] = div_n((double)v.n_heavy, dn, g.rn);
     out.fid[r] = v.fid;
     out.lat[r] = v.lat;
     out.cell[r] = (uint32_t)c;
@@ -1709,7 +1722,8 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * 8, st));
 
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
-         n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted};
+         n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted,
+         1.0 / (double)n};
   int launches = 31;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
