@@ -233,7 +233,10 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     backend = os.environ.get("HADIS_DIST_BACKEND", "nccl")   # gloo: multi-rank tests on 1 GPU
-    if world > 1:
+    # HADIS_BENCH_SHARDED=1: the N > 1 code path (process group, slabs, all-gather,
+    # merge kernel) even at world 1 -- exercises NCCL on a one-GPU box
+    dist_on = world > 1 or os.environ.get("HADIS_BENCH_SHARDED") == "1"
+    if dist_on:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -247,7 +250,7 @@ def run_ours(args, cfg):
     d_h = h_pin.to(dev)
     # pinned host copies for the e2e leg; resident device copies for `value`
     sharded = None
-    if world > 1:
+    if dist_on:
         # whole light-model groups per rank; the rank holds only its light
         # models' score rows (compact, slot-mapped).  Every step = local build
         # (CUDA graph) + one all-gather of the fixed-size slabs + the merge
@@ -289,7 +292,7 @@ def run_ours(args, cfg):
     rows = int(last["pair"].shape[0])
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -346,7 +349,7 @@ def run_ours(args, cfg):
     d2h = 0
     barrier()
     e2e_steps = max(3, min(args.steps, 8))
-    if plan is not None and world == 1:
+    if plan is not None and not dist_on:
         from paper_2509_00642_b200.profiler import TablePipeline
         pipe = TablePipeline(pool, n, sc_pin.shape[0], thr, pairs=mine, device=dev,
                              score_slots=slots if world > 1 else None)
@@ -384,7 +387,7 @@ def run_ours(args, cfg):
     # ---- max over ranks
     vals = torch.tensor([ms, statistics.median(e2e_ms), ms_b], dtype=torch.float64,
                         device=dev if backend == "nccl" else "cpu")
-    if world > 1:
+    if dist_on:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms_max, e2e_max, _ = vals.tolist()
 
@@ -402,7 +405,7 @@ def run_ours(args, cfg):
             "config": {"workload": cfg.name, "models": cfg.n_models, "pairs": cfg.n_pairs,
                        "queries": n, "thresholds": cfg.k, "cells": cfg.cells, "rows": rows,
                        "parallelism": f"pair-shard x{world} + one all-gather merge per step"
-                       if world > 1 else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
+                       if dist_on else "single gpu", "l2": "inputs (8*N*(1+L) bytes) exceed the 126 MB L2"},
             "table_build_ms": ms_max,
             # per-stage CUDA events of an eager launch; the eager frontier span also
             # holds host launch gaps, so the in-graph frontier time is derived too
@@ -423,7 +426,7 @@ def run_ours(args, cfg):
             "gpu_launches": int(launches),
             "clocks": sampler.summary(),
         }
-        if world == 1:
+        if not dist_on:
             line["materialise"] = measure_materialise(last_dt, pool, thr)
         if not args.no_allocation:
             line["allocation_search"] = measure_allocation(torch, dev, args.steps)
@@ -445,7 +448,7 @@ def run_ours(args, cfg):
                                               " 146-147)",
                                     "host_cores": os.cpu_count()}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 

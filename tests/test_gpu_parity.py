@@ -883,3 +883,12 @@ def test_bench_multi_rank_line(gpu_device):
     assert l2["n_gpus"] == 2 and l2["value"] > 0 and l2["ms_per_step"] > 0
     assert l2["config"]["rows"] == l1["config"]["rows"]
     assert "merge" in l2 and l2["merge"]["row_bytes"] == 44
+    # the same sharded step over NCCL (one rank: process group, all-gather of the
+    # slab, merge kernel) -- the collective path the multi-GPU runs take
+    env = dict(os.environ, HADIS_BENCH_SHARDED="1", HADIS_DIST_BACKEND="nccl")
+    nccl = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                           "--nproc-per-node", "1", os.path.join(root, "bench.py")] + args,
+                          capture_output=True, text=True, env=env, timeout=900)
+    assert nccl.returncode == 0, nccl.stderr[-3000:]
+    l3 = json.loads([x for x in nccl.stdout.splitlines() if x.startswith("{")][-1])
+    assert l3["config"]["rows"] == l1["config"]["rows"] and "merge" in l3
