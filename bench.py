@@ -307,7 +307,8 @@ def run_ours(args, cfg):
                                     "the slab header: no count round trip)",
                       "slab_bytes": sharded.slab.nbytes, "rows_capacity": sharded.slab.cap,
                       "bytes_received_per_rank": sharded.gather_bytes,
-                      "row_bytes": 44, "merge_kernel_ms": e0.elapsed_time(e1)}
+                      "slab_row_bytes": 24, "table_row_bytes": 44,
+                      "merge_kernel_ms": e0.elapsed_time(e1)}
 
     # ---- per-stage CUDA events (eager launches, same work) for stage_ms / roofline
     kev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]

@@ -170,6 +170,20 @@ int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int6
                          int32_t* out_pair, int32_t* out_theta_pos, int32_t* out_tau_pos,
                          double* out_r_light, double* out_r_heavy, double* out_fid,
                          double* out_lat, int64_t* stats, void* stream);
+/* The same frontier with compact rows (the multi-GPU slab, 24 bytes per row):
+ * theta_pos, tau_pos, fid as above, n_light = records the light stage serves
+ * (r_light * n), n_heavy = records the heavy stage serves (r_heavy * n); the
+ * pair of a row is implied by the per-pair row counts in stats. */
+int hadis_pair_frontiers_compact(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
+                                 int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
+                                 const int32_t* pair_slot, const double* pair_params,
+                                 const int32_t* first_pos, int32_t n_thresholds,
+                                 const double* thr_unique, const double* h,
+                                 const double* scores, int32_t exact_fid, void* workspace,
+                                 size_t workspace_bytes, int64_t cand_cap, int64_t exact_cap,
+                                 int64_t out_cap, int32_t* out_theta_pos, int32_t* out_tau_pos,
+                                 uint32_t* out_n_light, uint32_t* out_n_heavy, double* out_fid,
+                                 int64_t* stats, void* stream);
 
 /* numpy-exact mean of where(h > theta | s < tau, cost_heavy, cost_light)
  * (profiler.py:152-153) for n_cells cells: cell c uses score row
@@ -205,27 +219,32 @@ int hadis_cascade_points(const double* h, const double* scores, int64_t n, int32
 /* Multi-GPU merge of pair-sharded tables (SURVEY §8 e)     */
 /* ------------------------------------------------------------------------- */
 
-/* A rank's "slab": int64 header[hdr_words] then the seven row columns of
- * hadis_pair_frontiers at native width -- pair, theta_pos, tau_pos (int32[cap]
- * each, back to back from byte 8*hdr_words), then r_light, r_heavy, fid, lat
- * (float64[cap] each, from the next 8-byte boundary).  The header holds the
- * frontier's stats array for the rank's local pairs (HADIS_ST_*, per-local-pair
- * row counts at HADIS_ST_PAIR0 + j, the record-validation flag right after
- * them) and a host error word at hdr_words - 1.  The frontier pass writes
- * straight into these columns (no pack step). */
+/* A rank's "slab": int64 header[hdr_words] then the compact rows of
+ * hadis_pair_frontiers_compact -- theta_pos, tau_pos (int32[cap]), n_light,
+ * n_heavy (uint32[cap]), back to back from byte 8*hdr_words, then fid
+ * (float64[cap], from the next 8-byte boundary): 24 bytes per row.  The header
+ * holds the frontier's stats array for the rank's local pairs (HADIS_ST_*,
+ * per-local-pair row counts at HADIS_ST_PAIR0 + j, the record-validation flag
+ * right after them) and a host error word at hdr_words - 1.  The frontier pass
+ * writes straight into these columns (no pack step). */
 size_t hadis_shard_slab_bytes(int32_t hdr_words, int64_t cap);
 size_t hadis_shard_merge_workspace_bytes(int32_t n_pairs);
 
 /* gathered = world slabs back to back (all_gather_into_tensor of the slabs),
  * global pair g owned by rank pair_rank[g] as its local pair pair_local[g];
- * rank r holds rank_npairs[r] pairs.  Writes the canonical table (pairs in
- * global order, rows of a pair in the owner's (theta, tau) order, pair column
- * = global id) and out_stats[5] = {total rows, OR of overflow bits (8 = a slab
- * or out_cap overflowed), OR of record flags, OR of host error words, max rows
- * of one rank}.  Rows are copied only when all three status words are 0. */
+ * rank r holds rank_npairs[r] pairs; pair_params = the global pairs'
+ * hadis_pair_frontiers parameters ([n_pairs][HADIS_PAIR_PARAMS], device), n =
+ * the record count.  Writes the canonical table (pairs in global order, rows
+ * of a pair in the owner's (theta, tau) order, pair column = global id;
+ * r_light, r_heavy, lat rebuilt from n_light / n_heavy bit-identically to
+ * hadis_pair_frontiers) and out_stats[5] = {total rows, OR of overflow bits (8
+ * = a slab or out_cap overflowed), OR of record flags, OR of host error words,
+ * max rows of one rank}.  Rows are copied only when all three status words
+ * are 0. */
 int hadis_shard_merge(const void* gathered, int32_t world, size_t slab_bytes, int64_t cap,
                       int32_t hdr_words, const int32_t* pair_rank, const int32_t* pair_local,
-                      const int32_t* rank_npairs, int32_t n_pairs, int64_t out_cap,
+                      const int32_t* rank_npairs, int32_t n_pairs, const double* pair_params,
+                      int64_t n, int64_t out_cap,
                       int32_t* out_pair, int32_t* out_theta_pos, int32_t* out_tau_pos,
                       double* out_r_light, double* out_r_heavy, double* out_fid,
                       double* out_lat, int64_t* out_stats, void* workspace,

@@ -50,6 +50,10 @@ _SIGNATURES = {
                                       _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_i32, _c_vp, _c_sz,
                                       _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
                                       _c_vp, _c_vp, _c_vp, _c_vp]),
+    "hadis_pair_frontiers_compact": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_vp,
+                                              _c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_i32,
+                                              _c_vp, _c_sz, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp,
+                                              _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
     "hadis_fid_exact": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
                                  _c_vp]),
     "hadis_cascade_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
@@ -58,8 +62,8 @@ _SIGNATURES = {
     "hadis_shard_slab_bytes": (_c_sz, [_c_i32, _c_i64]),
     "hadis_shard_merge_workspace_bytes": (_c_sz, [_c_i32]),
     "hadis_shard_merge": (_c_int, [_c_vp, _c_i32, _c_sz, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp,
-                                   _c_i32, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp,
-                                   _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
+                                   _c_i32, _c_vp, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_vp,
+                                   _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_sz, _c_vp]),
     "hadis_lexicon_bytes": (_c_sz, []),
     "hadis_text_workspace_bytes": (_c_sz, [_c_i64]),
     "hadis_text_records": (_c_int, [_c_vp, _c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_i32, _c_vp,

@@ -1478,11 +1478,13 @@ struct Rows {
   int32_t* pair;
   int32_t* theta_pos;
   int32_t* tau_pos;
-  double* r_light;
-  double* r_heavy;
+  double* r_light;  // null in the compact form (multi-GPU slab): rebuilt from
+  double* r_heavy;  // n_light / n_heavy by the merge, bit for bit
   double* fid;
   double* lat;
   uint32_t* cell;   // workspace: k * U + t, for exact patches
+  uint32_t* n_light;   // compact form only: R_k (records the light stage serves)
+  uint32_t* n_heavy;   // compact form only: nb + nr (records the heavy stage serves)
 };
 
 // bits -> cell list in shared memory -> one row per thread (coalesced stores)
@@ -1517,11 +1519,16 @@ emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __re
     out.pair[r] = p;
     out.theta_pos[r] = g.first_pos[k];
     out.tau_pos[r] = g.first_pos[t];
-    out.r_light[r] = div_n((double)v.n_keep_light, dn, g.rn);
-    out.r_heavy[r] = div_n((double)v.n_heavy, dn, g.rn);
     out.fid[r] = v.fid;
-    out.lat[r] = v.lat;
     out.cell[r] = (uint32_t)c;
+    if (out.n_light != nullptr) {                  // compact rows (uniform branch)
+      out.n_light[r] = v.n_keep_light;
+      out.n_heavy[r] = v.n_heavy;
+    } else {
+      out.r_light[r] = div_n((double)v.n_keep_light, dn, g.rn);
+      out.r_heavy[r] = div_n((double)v.n_heavy, dn, g.rn);
+      out.lat[r] = v.lat;
+    }
   }
 }
 
@@ -1576,7 +1583,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 struct Layout {
   size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
       counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell,
-      rsort[5], rsort_bytes, total;
+      row_pair, rsort[5], rsort_bytes, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1621,6 +1628,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.ctsum = take(8 * (ceil_div(n_cw, 4096) + 1));
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
+  L.row_pair = take(4 * out_cap);                  // compact outputs: pair ids of the rows
   if (ecap > kSortMax) {                           // CUB request sort (see pack_requests_kernel)
     L.rsort[0] = take(8 * ecap); L.rsort[1] = take(8 * ecap);     // keys in / out
     L.rsort[2] = take(8 * ecap); L.rsort[3] = take(8 * ecap);     // fid in / out
@@ -1652,21 +1660,25 @@ extern "C" size_t hadis_frontier_workspace_bytes(int32_t n_pairs, int32_t n_uniq
   return make_layout(n_pairs, n_unique, buckets_for(n_unique), cand_cap, exact_cap, out_cap).total;
 }
 
-extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
-                                    int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
-                                    const int32_t* pair_slot, const double* pair_params,
-                                    const int32_t* first_pos, int32_t n_thresholds,
-                                    const double* thr_unique, const double* h,
-                                    const double* scores, int32_t exact_fid, void* workspace,
-                                    size_t workspace_bytes, int64_t cand_cap, int64_t exact_cap,
-                                    int64_t out_cap, int32_t* out_pair, int32_t* out_theta_pos,
-                                    int32_t* out_tau_pos, double* out_r_light,
-                                    double* out_r_heavy, double* out_fid, double* out_lat,
-                                    int64_t* stats, void* stream) {
+// Shared body of hadis_pair_frontiers (full rows) and hadis_pair_frontiers_compact
+// (out_n_light != null: theta_pos, tau_pos, n_light, n_heavy, fid only).
+static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
+                          int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
+                          const int32_t* pair_slot, const double* pair_params,
+                          const int32_t* first_pos, int32_t n_thresholds,
+                          const double* thr_unique, const double* h, const double* scores,
+                          int32_t exact_fid, void* workspace, size_t workspace_bytes,
+                          int64_t cand_cap, int64_t exact_cap, int64_t out_cap, int32_t* out_pair,
+                          int32_t* out_theta_pos, int32_t* out_tau_pos, double* out_r_light,
+                          double* out_r_heavy, double* out_fid, double* out_lat,
+                          uint32_t* out_n_light, uint32_t* out_n_heavy, int64_t* stats,
+                          void* stream) {
   if (!pre_cnt || !pre_hsum || n <= 0 || n > 0xffffffffll || n_unique <= 0 ||
       n_unique > kMaxRowU || n_pairs <= 0 || !pair_slot || !pair_params || !first_pos ||
       n_thresholds < n_unique || !thr_unique || !h || !scores || !workspace || cand_cap <= 0 ||
-      exact_cap <= 0 || out_cap <= 0 || !stats)
+      exact_cap <= 0 || out_cap <= 0 || !stats || !out_theta_pos || !out_tau_pos || !out_fid)
+    return HADIS_ERR_ARG;
+  if (out_n_light ? !out_n_heavy : (!out_pair || !out_r_light || !out_r_heavy || !out_lat))
     return HADIS_ERR_ARG;
   if ((int64_t)n_unique * n_unique > 0xffffffffll) return HADIS_ERR_UNSUPPORTED;
   const int nb = buckets_for(n_unique);
@@ -1709,6 +1721,7 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   unsigned long long* ctsum = (unsigned long long*)P(L.ctsum);
   unsigned long long* pair_off = (unsigned long long*)P(L.pair_off);
   uint32_t* row_cell = (uint32_t*)P(L.row_cell);
+  int32_t* row_pair = (int32_t*)P(L.row_pair);
 
   const int64_t pb = (int64_t)n_pairs * nb;
   const int64_t cells = (int64_t)n_unique * n_unique;
@@ -1857,8 +1870,9 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   }
   pair_offsets_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       chunk_off, n_chunks, n_pairs, pair_off, stats, out_cap, counters);
-  Rows out{out_pair, out_theta_pos, out_tau_pos, out_r_light, out_r_heavy, out_fid, out_lat,
-           row_cell};
+  if (out_n_light != nullptr) out_pair = row_pair;   // compact: pair ids stay in the workspace
+  Rows out{out_pair,    out_theta_pos, out_tau_pos, out_r_light, out_r_heavy,
+           out_fid,     out_lat,       row_cell,    out_n_light, out_n_heavy};
   emit_rows_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(
       g, pcs, kept, words_per_pair, n_chunks, chunk_off, out_cap, out);
   if (exact_fid) {
@@ -1881,6 +1895,40 @@ extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre
   HADIS_LAUNCH_CHECK();
   hadis_count_launches(exact_fid ? launches - 1 : launches);
   return HADIS_OK;
+}
+
+extern "C" int hadis_pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n,
+                                    int32_t n_unique, int32_t hfix_shift, int32_t n_pairs,
+                                    const int32_t* pair_slot, const double* pair_params,
+                                    const int32_t* first_pos, int32_t n_thresholds,
+                                    const double* thr_unique, const double* h,
+                                    const double* scores, int32_t exact_fid, void* workspace,
+                                    size_t workspace_bytes, int64_t cand_cap, int64_t exact_cap,
+                                    int64_t out_cap, int32_t* out_pair, int32_t* out_theta_pos,
+                                    int32_t* out_tau_pos, double* out_r_light,
+                                    double* out_r_heavy, double* out_fid, double* out_lat,
+                                    int64_t* stats, void* stream) {
+  return pair_frontiers(pre_cnt, pre_hsum, n, n_unique, hfix_shift, n_pairs, pair_slot,
+                        pair_params, first_pos, n_thresholds, thr_unique, h, scores, exact_fid,
+                        workspace, workspace_bytes, cand_cap, exact_cap, out_cap, out_pair,
+                        out_theta_pos, out_tau_pos, out_r_light, out_r_heavy, out_fid, out_lat,
+                        nullptr, nullptr, stats, stream);
+}
+
+extern "C" int hadis_pair_frontiers_compact(
+    const uint32_t* pre_cnt, const uint64_t* pre_hsum, int64_t n, int32_t n_unique,
+    int32_t hfix_shift, int32_t n_pairs, const int32_t* pair_slot, const double* pair_params,
+    const int32_t* first_pos, int32_t n_thresholds, const double* thr_unique, const double* h,
+    const double* scores, int32_t exact_fid, void* workspace, size_t workspace_bytes,
+    int64_t cand_cap, int64_t exact_cap, int64_t out_cap, int32_t* out_theta_pos,
+    int32_t* out_tau_pos, uint32_t* out_n_light, uint32_t* out_n_heavy, double* out_fid,
+    int64_t* stats, void* stream) {
+  if (!out_n_light) return HADIS_ERR_ARG;
+  return pair_frontiers(pre_cnt, pre_hsum, n, n_unique, hfix_shift, n_pairs, pair_slot,
+                        pair_params, first_pos, n_thresholds, thr_unique, h, scores, exact_fid,
+                        workspace, workspace_bytes, cand_cap, exact_cap, out_cap, nullptr,
+                        out_theta_pos, out_tau_pos, nullptr, nullptr, out_fid, nullptr,
+                        out_n_light, out_n_heavy, stats, stream);
 }
 
 extern "C" int hadis_fid_exact(const double* h, const double* scores, int64_t n, int32_t n_cells,

@@ -479,13 +479,20 @@ class GridProfiler:
                        lat=torch.empty(out_cap, dtype=torch.float64, device=dev))
             stats = torch.zeros(_lib.ST_PAIR0 + P + 1, dtype=torch.int64, device=dev)  # + bad
         p = _lib.ptr
-        _lib.check(self.lib.hadis_pair_frontiers(
-            p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(plan.d_slot),
-            p(plan.d_params), p(plan.d_first), len(plan.grid.thresholds), p(plan.d_u),
-            p(self.h), p(state["scores"]), 1 if state["exact_fid"] else 0, p(self._ws), ws_bytes,
-            cand_cap, exact_cap, out_cap, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]),
-            p(out["r_light"]), p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
-            _lib.stream_handle(state["stream"], self.device)), "hadis_pair_frontiers")
+        args = (p(state["cnt"]), p(state["hsum"]), self.n, U, self.shift, P, p(plan.d_slot),
+                p(plan.d_params), p(plan.d_first), len(plan.grid.thresholds), p(plan.d_u),
+                p(self.h), p(state["scores"]), 1 if state["exact_fid"] else 0, p(self._ws),
+                ws_bytes, cand_cap, exact_cap, out_cap)
+        if self.sink is not None:           # compact rows (the merge rebuilds the rest)
+            _lib.check(self.lib.hadis_pair_frontiers_compact(
+                *args, p(out["theta_pos"]), p(out["tau_pos"]), p(out["n_light"]),
+                p(out["n_heavy"]), p(out["fid"]), p(stats),
+                _lib.stream_handle(state["stream"], self.device)), "hadis_pair_frontiers_compact")
+        else:
+            _lib.check(self.lib.hadis_pair_frontiers(
+                *args, p(out["pair"]), p(out["theta_pos"]), p(out["tau_pos"]), p(out["r_light"]),
+                p(out["r_heavy"]), p(out["fid"]), p(out["lat"]), p(stats),
+                _lib.stream_handle(state["stream"], self.device)), "hadis_pair_frontiers")
         # the record-validation flag rides along, so finish() needs one device read
         with torch.cuda.stream(state["stream"] or torch.cuda.current_stream(self.device)):
             stats[-1:].copy_(self.bad)
@@ -519,12 +526,12 @@ class GridProfiler:
             raise ProfileError("profile_records: capacity retries exhausted")
         n_rows = stats[_lib.ST_ROWS]
         out = state["out"]
+        col = (lambda f: out[f][:n_rows] if f in out else None)   # slab sinks hold compact rows
         return DeviceTable(
             pairs=plan.pairs, n_rows=n_rows,
             pair_rows=stats[_lib.ST_PAIR0:_lib.ST_PAIR0 + plan.P],
-            pair=out["pair"][:n_rows], theta_pos=out["theta_pos"][:n_rows],
-            tau_pos=out["tau_pos"][:n_rows], r_light=out["r_light"][:n_rows],
-            r_heavy=out["r_heavy"][:n_rows], fid=out["fid"][:n_rows], lat=out["lat"][:n_rows],
+            pair=col("pair"), theta_pos=col("theta_pos"), tau_pos=col("tau_pos"),
+            r_light=col("r_light"), r_heavy=col("r_heavy"), fid=col("fid"), lat=col("lat"),
             stats={"rows": n_rows, "candidates": stats[_lib.ST_CANDIDATES],
                    "uncertain": stats[_lib.ST_UNCERTAIN],
                    "exact_cells": stats[_lib.ST_EXACT_CELLS]})

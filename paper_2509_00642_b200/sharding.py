@@ -9,14 +9,16 @@ deterministic (pair, theta, tau) reduction order.  One process per GPU:
   light models; ``shard_pairs`` is the plain contiguous split;
 * each rank builds its pairs' frontiers with no data-path collective (a
   pair's frontier needs no other pair's cells), emitting rows straight into
-  its slab (``ShardSlab``: frontier stats header + the seven row columns at
-  native 44 bytes per row -- no pack step);
+  its slab (``ShardSlab``: frontier stats header + the compact rows of
+  ``hadis_pair_frontiers_compact`` -- theta_pos, tau_pos, n_light, n_heavy,
+  fid: 24 bytes per row instead of the table's 44, no pack step);
 * one ``all_gather_into_tensor`` of the fixed-size slabs (NCCL over NVLink on
   GPUs; gloo moves them through host memory) gives every rank every slab,
   row counts included, so no count round trip precedes it;
 * ``hadis_shard_merge`` writes the canonical table on every rank (pairs in
-  global order, each pair's rows in its owner's (theta, tau) order) without a
-  host round trip; the table is identical for 1/2/4/8 GPUs.
+  global order, each pair's rows in its owner's (theta, tau) order; r_light,
+  r_heavy, lat rebuilt from the counts with the frontier's own operations)
+  without a host round trip; the table is identical for 1/2/4/8 GPUs.
 
 Error consensus: a rank's local failure (bad records, a slab too small, an
 exception) is written into its slab header instead of being raised before
@@ -35,6 +37,7 @@ from . import _lib
 
 FIELDS = ("pair", "theta_pos", "tau_pos", "r_light", "r_heavy", "fid", "lat")
 _INT_FIELDS = ("pair", "theta_pos", "tau_pos")
+SLAB_FIELDS = ("theta_pos", "tau_pos", "n_light", "n_heavy", "fid")   # compact slab rows
 
 ERR_RECORDS, ERR_SLAB, ERR_PROFILE = 1, 2, 4       # host error word bits
 
@@ -110,12 +113,13 @@ class ShardSlab:
         return slab_offsets(self.hdr_words, self.cap)
 
     def columns(self, out_cap=None):
+        """Views of the compact row columns (n_light / n_heavy hold uint32 bits)."""
         if out_cap is not None and out_cap != self.cap:
             raise ValueError("ShardSlab: the frontier's out_cap must equal the slab capacity")
         torch, cap = self.torch, self.cap
         out = {}
-        for f, off in zip(FIELDS, self.offsets()):
-            dt, size = (torch.int32, 4) if f in _INT_FIELDS else (torch.float64, 8)
+        for f, off in zip(SLAB_FIELDS, self.offsets()):
+            dt, size = (torch.float64, 8) if f == "fid" else (torch.int32, 4)
             out[f] = self.buf[off:off + size * cap].view(dt)
         return out
 
@@ -127,10 +131,10 @@ class ShardSlab:
 
 
 def slab_offsets(hdr_words: int, cap: int):
-    """Byte offsets of the seven columns (csrc/shards.cu slab_i32_off / slab_f64_off)."""
-    i32 = [8 * hdr_words + 4 * k * cap for k in range(3)]
-    f0 = (8 * hdr_words + 12 * cap + 7) & ~7
-    return i32 + [f0 + 8 * k * cap for k in range(4)]
+    """Byte offsets of the compact columns SLAB_FIELDS (csrc/shards.cu slab_i32_off /
+    slab_f64_off): four 32-bit columns back to back, then fid at an 8-byte boundary."""
+    i32 = [8 * hdr_words + 4 * k * cap for k in range(4)]
+    return i32 + [(8 * hdr_words + 16 * cap + 7) & ~7]
 
 
 def all_gather_slab(torch, dist, slab_buf, gathered, group=None):
@@ -171,6 +175,9 @@ class ShardedTable:
         self.d_pair_rank = torch.from_numpy(self.map.pair_rank).to(dev)
         self.d_pair_local = torch.from_numpy(self.map.pair_local).to(dev)
         self.d_rank_npairs = torch.from_numpy(self.map.rank_npairs).to(dev)
+        from .profiler import pair_params
+        self.d_params = torch.from_numpy(pair_params(self.pool, self.pairs)).to(dev)
+        self.n_records = int(h.shape[0]) if hasattr(h, "shape") else len(h)
         self.out_stats = torch.zeros(8, dtype=torch.int64, device=dev)
         self.stats_pin = torch.zeros(8, dtype=torch.int64).pin_memory()
         self.hdr_pin = torch.zeros(self.map.hdr_words, dtype=torch.int64).pin_memory()
@@ -298,6 +305,7 @@ class ShardedTable:
         _lib.check(self.lib.hadis_shard_merge(
             p(self.gathered), self.world, self.slab.nbytes, self.slab.cap, self.map.hdr_words,
             p(self.d_pair_rank), p(self.d_pair_local), p(self.d_rank_npairs), len(self.pairs),
+            p(self.d_params), self.n_records,
             self.out_cap, p(m["pair"]), p(m["theta_pos"]), p(m["tau_pos"]), p(m["r_light"]),
             p(m["r_heavy"]), p(m["fid"]), p(m["lat"]), p(self.out_stats), p(self.ws),
             self.ws.numel(), _lib.stream_handle(stream, self.device)), "hadis_shard_merge")

@@ -882,7 +882,7 @@ def test_bench_multi_rank_line(gpu_device):
     l2 = json.loads([x for x in two.stdout.splitlines() if x.startswith("{")][-1])
     assert l2["n_gpus"] == 2 and l2["value"] > 0 and l2["ms_per_step"] > 0
     assert l2["config"]["rows"] == l1["config"]["rows"]
-    assert "merge" in l2 and l2["merge"]["row_bytes"] == 44
+    assert "merge" in l2 and l2["merge"]["slab_row_bytes"] == 24
     # the same sharded step over NCCL (one rank: process group, all-gather of the
     # slab, merge kernel) -- the collective path the multi-GPU runs take
     env = dict(os.environ, HADIS_BENCH_SHARDED="1", HADIS_DIST_BACKEND="nccl")

@@ -2,7 +2,9 @@
 covers every pair once in canonical order; slabs laid out as the C ABI
 defines them (hadis_shard_slab_bytes) travel through the product's
 all-gather, and a numpy mirror of hadis_shard_merge over the gathered bytes
-reproduces the canonical row list exactly.  (The CUDA merge itself runs in
+reproduces the canonical row list exactly, r_light / r_heavy / lat rebuilt
+from the compact rows' counts as IEEE divisions by n (what the kernel's div_n
+computes).  (The CUDA merge itself runs in
 the GPU test test_sharded_profile_equals_single.)"""
 
 import os
@@ -16,8 +18,15 @@ import torch.multiprocessing as mp
 import numpy as np
 
 from paper_2509_00642_b200 import _lib
-from paper_2509_00642_b200.sharding import (FIELDS, ShardMap, all_gather_slab, shard_light_groups,
-                                            shard_pairs, slab_offsets)
+from paper_2509_00642_b200.sharding import (FIELDS, SLAB_FIELDS, ShardMap, all_gather_slab,
+                                            shard_light_groups, shard_pairs, slab_offsets)
+
+N_REC = 1000003          # record count of the fake slabs
+
+
+def _lat_pair(g):
+    """Fake (L_light, L_heavy) of global pair g."""
+    return 0.25 + g / 13.0, 1.5 + g / 7.0
 
 
 def _free_port():
@@ -59,9 +68,17 @@ def test_shard_light_groups_partition(models, world):
 
 
 def _rows_for(g):
-    """Deterministic fake rows of global pair g: g % 3 + 1 rows."""
-    return [(k, 2 * k + 1, g / 7.0 + k, 1.0 / (g + k + 1), 30.0 - g * 0.01 - k / 3.0,
-             0.5 + g + k * 1e-3) for k in range(g % 3 + 1)]
+    """Deterministic fake compact rows of global pair g: g % 3 + 1 rows of
+    (theta_pos, tau_pos, n_light, n_heavy, fid)."""
+    return [(k, 2 * k + 1, N_REC - 17 * g - k, 3 * g + 11 * k + 1, 30.0 - g * 0.01 - k / 3.0)
+            for k in range(g % 3 + 1)]
+
+
+def _table_row(g, row):
+    """The table row the merge must produce from a compact row (profiler order)."""
+    th, ta, nl, nh, fid = row
+    ll, lh = _lat_pair(g)
+    return (th, ta, nl / N_REC, nh / N_REC, fid, (nl * ll + nh * lh) / N_REC)
 
 
 def _fake_slab(smap, rank, cap):
@@ -70,16 +87,15 @@ def _fake_slab(smap, rank, cap):
     buf = np.zeros(nbytes, dtype=np.uint8)
     hdr = buf[:8 * hw].view(np.int64)
     offs = slab_offsets(hw, cap)
-    cols = [buf[offs[k]:offs[k] + 4 * cap].view(np.int32) for k in range(3)] + \
-        [buf[offs[3 + k]:offs[3 + k] + 8 * cap].view(np.float64) for k in range(4)]
+    cols = [buf[offs[k]:offs[k] + 4 * cap].view(np.uint32 if k >= 2 else np.int32)
+            for k in range(4)] + [buf[offs[4]:offs[4] + 8 * cap].view(np.float64)]
     r = 0
     for j, g in enumerate(smap.rank_ids[rank]):
         rows = _rows_for(g)
         hdr[_lib.ST_PAIR0 + j] = len(rows)
         for row in rows:
-            cols[0][r] = j                                   # local pair id
             for k, v in enumerate(row):
-                cols[1 + k][r] = v
+                cols[k][r] = v
             r += 1
     hdr[_lib.ST_ROWS] = r
     return buf
@@ -97,11 +113,18 @@ def _merge_mirror(gathered, smap, cap):
         hdr = slab[:8 * hw].view(np.int64)
         src = int(hdr[_lib.ST_PAIR0:_lib.ST_PAIR0 + j].sum())
         cnt = int(hdr[_lib.ST_PAIR0 + j])
-        cols = [slab[offs[k]:offs[k] + 4 * cap].view(np.int32) for k in range(3)] + \
-            [slab[offs[3 + k]:offs[3 + k] + 8 * cap].view(np.float64) for k in range(4)]
-        out["pair"] += [g] * cnt
-        for k, f in enumerate(FIELDS[1:]):
-            out[f] += cols[1 + k][src:src + cnt].tolist()
+        cols = [slab[offs[k]:offs[k] + 4 * cap].view(np.uint32 if k >= 2 else np.int32)
+                for k in range(4)] + [slab[offs[4]:offs[4] + 8 * cap].view(np.float64)]
+        ll, lh = _lat_pair(g)
+        for i in range(src, src + cnt):
+            th, ta, nl, nh, fid = (c[i].item() for c in cols)
+            out["pair"].append(g)
+            out["theta_pos"].append(th)
+            out["tau_pos"].append(ta)
+            out["r_light"].append(float(nl) / N_REC)      # IEEE division = the kernel's div_n
+            out["r_heavy"].append(float(nh) / N_REC)
+            out["fid"].append(fid)
+            out["lat"].append((float(nl) * ll + float(nh) * lh) / N_REC)
     return out
 
 
@@ -130,7 +153,7 @@ def test_slab_gather_and_merge_gloo_world2(tmp_path, n_models):
         for row in _rows_for(g):
             want["pair"].append(g)
             for k, f in enumerate(FIELDS[1:]):
-                want[f].append(row[k])
+                want[f].append(_table_row(g, row)[k])
     for f in FIELDS:
         assert merged[f] == want[f], f
 
@@ -151,5 +174,6 @@ def test_slab_layout_matches_library(cap):
     hw = 160
     nbytes = _lib.load().hadis_shard_slab_bytes(hw, cap)
     offs = slab_offsets(hw, cap)
-    assert offs[0] == 8 * hw and all(o % 8 == 0 for o in offs[3:])
+    assert len(offs) == len(SLAB_FIELDS) == 5
+    assert offs[0] == 8 * hw and offs[4] % 8 == 0 and offs[4] >= offs[3] + 4 * cap
     assert offs[-1] + 8 * cap <= nbytes and nbytes % 256 == 0
