@@ -660,6 +660,9 @@ __device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* f
       x[2 * p] = v.x;
       x[2 * p + 1] = v.y;
     }
+    // order this thread's generic-proxy reads of the slot before the async-proxy
+    // (bulk copy) writes the producer issues once the empty barrier completes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive_u32(empty0 + 8 * slot);
     if (++slot == kTmaSlots) { slot = 0; ph ^= 1u; }
