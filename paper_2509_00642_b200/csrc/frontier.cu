@@ -295,27 +295,108 @@ __global__ void __launch_bounds__(1024)
 row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
                    const int32_t* __restrict__ first_pos, int32_t* pk, int32_t* row_rep,
                    uint8_t* row_start, int32_t* sorted) {
-  extern __shared__ uint32_t s_R[];
+  // Classes are runs of equal R.  Each thread owns a contiguous segment of ranks;
+  // three block scans give every rank its run start a (max-scan of starts), its
+  // run end b (reverse min-scan of starts) and the run's first_pos-smallest rank
+  // (segmented min-scan of (first_pos, rank) keys, read at the run's last rank).
+  // (One walk per rank to its run's ends was O(run^2): 13 us at c4.)
+  extern __shared__ __align__(8) unsigned char rc_smem[];
+  long long* s_runmin = reinterpret_cast<long long*>(rc_smem);   // [U] min key over [a(k), k]
+  uint32_t* s_R = reinterpret_cast<uint32_t*>(s_runmin + U);      // [U]
   __shared__ int s_unsorted;
-  if (threadIdx.x == 0) s_unsorted = 0;
+  __shared__ long long s_w[32];
+  const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (U + T - 1) / T, k0 = min(U, tid * per), k1 = min(U, k0 + per);
+  if (tid == 0) s_unsorted = 0;
   __syncthreads();
-  for (int k = threadIdx.x; k < U; k += blockDim.x) {
+  for (int k = tid; k < U; k += T) {
     s_R[k] = cnt[(int64_t)k * B1 + U];
     if (k > 0 && first_pos[k] < first_pos[k - 1]) s_unsorted = 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0) *sorted = !s_unsorted;
-  // classes are runs of equal R; each rank walks to its run's ends
-  for (int k = threadIdx.x; k < U; k += blockDim.x) {
-    int a = k, b = k + 1;
-    while (a > 0 && s_R[a - 1] == s_R[k]) --a;
-    while (b < U && s_R[b] == s_R[k]) ++b;
-    int best = a;
-    for (int j = a + 1; j < b; ++j)
-      if (first_pos[j] < first_pos[best]) best = j;
-    row_rep[k] = best;
-    pk[k] = a - 1;
-    row_start[k] = k == a;
+  if (tid == 0) *sorted = !s_unsorted;
+  auto is_start = [&](int k) { return k == 0 || s_R[k - 1] != s_R[k]; };
+  // generic exclusive block scan over the thread totals (op: associative, id: identity)
+  auto block_excl = [&](long long v, long long id, auto op) {
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = op(x, y);
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      long long w = lane < (T >> 5) ? s_w[lane] : id;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w = op(w, y);
+      }
+      s_w[lane] = w;
+    }
+    __syncthreads();
+    long long e = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) e = id;
+    const long long pre = wid > 0 ? s_w[wid - 1] : id;
+    const long long r = op(pre, e);
+    __syncthreads();
+    return r;
+  };
+  auto mx = [](long long x, long long y) { return x > y ? x : y; };
+  auto mn = [](long long x, long long y) { return x < y ? x : y; };
+  // 1. run start a(k): last start <= k
+  long long t = -1;
+  for (int k = k0; k < k1; ++k) if (is_start(k)) t = k;
+  long long run_a = block_excl(t, -1, mx);
+  // 2. run end b(k): first start > k (reverse scan: threads in reverse order)
+  long long u = U;
+  for (int k = k1 - 1; k >= k0; --k) if (is_start(k)) u = k;
+  // exclusive min over higher threads = reverse exclusive scan: scan the mirrored thread ids
+  // (implemented as a min over all threads > tid through shared memory)
+  __shared__ int s_first_start[1024];
+  s_first_start[tid] = (int)u;
+  __syncthreads();
+  for (int o = 1; o < T; o <<= 1) {                 // suffix min across threads (log steps)
+    const int v = tid + o < T ? s_first_start[tid + o] : U;
+    __syncthreads();
+    if (v < s_first_start[tid]) s_first_start[tid] = v;
+    __syncthreads();
+  }
+  int run_b = tid + 1 < T ? s_first_start[tid + 1] : U;
+  // 3. segmented min of (first_pos << 32 | rank), restarted at run starts
+  const long long kInf = 0x7fffffffffffffffll;
+  long long seg = kInf;
+  bool has_start = false;
+  for (int k = k0; k < k1; ++k) {
+    const long long key = ((long long)first_pos[k] << 32) | (unsigned)k;
+    if (is_start(k)) { seg = key; has_start = true; } else seg = mn(seg, key);
+  }
+  // carry across threads: (has_start, seg) pairs combine as a segmented min
+  // encoded as "reset" flag in the top bit handled by two scans: the carry into a
+  // thread is the min over the preceding threads back to the last one with a start
+  __shared__ long long s_seg[1024];
+  __shared__ int s_has[1024];
+  s_seg[tid] = seg;
+  s_has[tid] = has_start;
+  __syncthreads();
+  long long carry = kInf;
+  for (int j = tid - 1; j >= 0; --j) {              // runs span few threads: short walk
+    carry = mn(carry, s_seg[j]);
+    if (s_has[j]) break;
+  }
+  // final pass: every rank's a, b and the run minimum
+  long long cur_a = run_a, cur = carry;
+  for (int k = k0; k < k1; ++k) {
+    const long long key = ((long long)first_pos[k] << 32) | (unsigned)k;
+    if (is_start(k)) { cur_a = k; cur = key; } else cur = mn(cur, key);
+    s_runmin[k] = cur;                              // min over [a(k), k]
+    pk[k] = (int32_t)cur_a - 1;
+    row_start[k] = is_start(k);
+  }
+  __syncthreads();
+  long long nb = run_b;
+  for (int k = k1 - 1; k >= k0; --k) {
+    if (k + 1 < U && is_start(k + 1)) nb = k + 1;
+    row_rep[k] = (int32_t)(s_runmin[nb - 1] & 0xffffffffll);
   }
 }
 
@@ -329,17 +410,26 @@ row_classes_kernel(const uint32_t* __restrict__ cnt, int U, int B1,
 __global__ void group_kernel(const int32_t* __restrict__ pair_slot, int n_pairs,
                              int32_t* __restrict__ group_p0, int32_t* __restrict__ n_groups,
                              unsigned long long* counters, int max_group) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  // one warp: group starts by ballot, 32 pairs per step (was one thread: 10 us)
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   int ng = 0;
-  for (int p = 0; p < n_pairs; ++p)
-    if (p == 0 || pair_slot[p] != pair_slot[p - 1]) group_p0[ng++] = p;
-  group_p0[ng] = n_pairs;
-  for (int i = 0; i < ng; ++i)
-    if (group_p0[i + 1] - group_p0[i] > max_group) {   // > 65 pool models: unsupported
-      counters[4] |= 128ull;
-      ng = 0;
-    }
-  *n_groups = ng;
+  for (int p0 = 0; p0 < n_pairs; p0 += 32) {
+    const int p = p0 + lane;
+    const bool start = p < n_pairs && (p == 0 || pair_slot[p] != pair_slot[p - 1]);
+    const unsigned m = __ballot_sync(0xffffffffu, start);
+    if (start) group_p0[ng + __popc(m & ((1u << lane) - 1u))] = p;
+    ng += __popc(m);
+  }
+  if (lane == 0) group_p0[ng] = n_pairs;
+  __syncwarp();
+  bool too_big = false;
+  for (int i = lane; i < ng; i += 32) too_big |= group_p0[i + 1] - group_p0[i] > max_group;
+  if (__any_sync(0xffffffffu, too_big)) {            // > 65 pool models: unsupported
+    if (lane == 0) counters[4] |= 128ull;
+    ng = 0;
+  }
+  if (lane == 0) *n_groups = ng;
 }
 
 struct __align__(16) Cand {
@@ -1221,23 +1311,29 @@ __device__ __forceinline__ int64_t cell_list_len(const CellList& cl) {
 
 constexpr int kPwRootThreads = 128;
 constexpr int kPwCellsPerLaunch = 16384;
+constexpr int64_t kPwRootGridY = 4 * kNumSMs;   // cells in flight per pw_roots launch
 
 // grid: (roots / kPwRootThreads, cells in this batch)
 __global__ void __launch_bounds__(kPwRootThreads)
 pw_roots_kernel(Grid g, const PairConst* __restrict__ pcs, const double* __restrict__ thr,
                 const double* __restrict__ h, const double* __restrict__ scores, CellList cl,
-                int64_t first, const PwPlan* __restrict__ plan, double* __restrict__ vals) {
-  const int64_t c = first + blockIdx.y;
-  if (c >= cell_list_len(cl)) return;
+                int64_t first, int64_t batch, const PwPlan* __restrict__ plan,
+                double* __restrict__ vals) {
+  // grid-stride over the batch's cells: the grid stays small when few (or no)
+  // cells need exact values -- the common case
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= plan->n_roots) return;
-  const int p = (int)cl.pair[c];
-  const uint32_t cell = cl.cell[c];
-  const PairConst pc = pcs[p];
-  const CellCost cc{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
+  const int64_t len = cell_list_len(cl);
   const int node = plan->root[r];
-  vals[(int64_t)blockIdx.y * kPwPlanNodes + node] =
-      pw_subtree(h, scores + (int64_t)pc.slot * g.n, plan->off[node], plan->len[node], cc);
+  for (int64_t j = blockIdx.y; j < batch && first + j < len; j += gridDim.y) {
+    const int64_t c = first + j;
+    const int p = (int)cl.pair[c];
+    const uint32_t cell = cl.cell[c];
+    const PairConst pc = pcs[p];
+    const CellCost cc{thr[cell / g.U], thr[cell % g.U], pc.bl, pc.pl, pc.bh, pc.ph};
+    vals[j * kPwPlanNodes + node] =
+        pw_subtree(h, scores + (int64_t)pc.slot * g.n, plan->off[node], plan->len[node], cc);
+  }
 }
 
 __global__ void pw_combine_kernel(CellList cl, int64_t first, const PwPlan* __restrict__ plan,
@@ -1434,23 +1530,31 @@ __global__ void resolve_kernel(Grid g, const PairConst* __restrict__ pcs,
 // come out pair-major and, within a pair, in (theta rank, tau rank) order.
 constexpr int kEmitWords = 256;   // = emit CTA size (64 / 128 / 512 measured: no gain)
 
-__global__ void __launch_bounds__(kScanThreads)
+// one warp per chunk (kEmitWords words, 8 per lane as two 16-byte loads), 8
+// chunks per CTA (one CTA per chunk and thread per word: 16 us at c4)
+constexpr int kCountWarps = 8;
+__global__ void __launch_bounds__(kCountWarps * 32)
 count_chunks_kernel(const uint32_t* __restrict__ kept_bm, int64_t words_per_pair, int n_chunks,
                     uint32_t* __restrict__ chunk_rows) {
-  const int p = blockIdx.y, c = blockIdx.x;
-  const int64_t wi = (int64_t)c * kEmitWords + threadIdx.x;
-  uint32_t v = wi < words_per_pair ? __popc(kept_bm[(int64_t)p * words_per_pair + wi]) : 0u;
+  static_assert(kEmitWords == 32 * 8, "8 words per lane");
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kCountWarps + (threadIdx.x >> 5), p = blockIdx.y;
+  if (c >= n_chunks) return;
+  const uint32_t* w = kept_bm + (int64_t)p * words_per_pair;
+  const int64_t w0 = (int64_t)c * kEmitWords + 4 * lane;
+  uint32_t v = 0;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  __shared__ uint32_t ws[32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t t = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0u;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if (threadIdx.x == 0) chunk_rows[(int64_t)p * n_chunks + c] = t;
+  for (int h = 0; h < 2; ++h) {
+    const int64_t wi = w0 + h * 128;
+    if (wi + 3 < words_per_pair && ((words_per_pair & 3) == 0)) {
+      const uint4 q = *reinterpret_cast<const uint4*>(w + wi);
+      v += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    } else {
+      for (int j = 0; j < 4; ++j) if (wi + j < words_per_pair) v += __popc(w[wi + j]);
+    }
   }
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (lane == 0) chunk_rows[(int64_t)p * n_chunks + c] = v;
 }
 
 __global__ void pair_offsets_kernel(const unsigned long long* __restrict__ chunk_off, int n_chunks,
@@ -1740,13 +1844,16 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   int launches = 31;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
-  row_classes_kernel<<<1, 1024, (size_t)n_unique * 4, st>>>(pre_cnt, n_unique, n_unique + 1,
+  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_classes_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)n_unique * 12)));
+  row_classes_kernel<<<1, 1024, (size_t)n_unique * 12, st>>>(pre_cnt, n_unique, n_unique + 1,
                                                             first_pos, pk, row_rep, row_start,
                                                             sorted);
   HADIS_LAUNCH_CHECK();
 
   const dim3 row_grid((unsigned)ceil_div(n_unique, kRowWarps), (unsigned)n_pairs);
-  group_kernel<<<1, 1, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups, counters, kMaxGroup);
+  group_kernel<<<1, 32, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups, counters, kMaxGroup);
   const size_t rsm = sizeof(RowSmem);
   const size_t fsm = rsm + (size_t)kRowWarps * kMaxGroup * 32;   // + per-window pass masks
   HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_min_kernel,
@@ -1829,8 +1936,9 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
     const CellList cl{req_pair, req_cell, counters + 2, nullptr, exact_cap};
     const int64_t batch = exact_cap < kPwCellsPerLaunch ? exact_cap : kPwCellsPerLaunch;
     for (int64_t first = 0; first < exact_cap; first += kPwCellsPerLaunch, launches += 2) {
-      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)batch), kPwRootThreads, 0,
-                        st>>>(g, pcs, thr_unique, h, scores, cl, first, pwplan, pwvals);
+      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)min(batch, kPwRootGridY)),
+                        kPwRootThreads, 0, st>>>(g, pcs, thr_unique, h, scores, cl, first, batch,
+                                                 pwplan, pwvals);
       pw_combine_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(cl, first, pwplan, pwvals,
                                                                         (double)n, req_fid);
     }
@@ -1860,8 +1968,8 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   HADIS_LAUNCH_CHECK();
   const int n_chunks = (int)ceil_div(words_per_pair, kEmitWords);
   const int64_t n_cw = (int64_t)n_chunks * n_pairs;
-  count_chunks_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(kept, words_per_pair,
-                                                                        n_chunks, chunk_rows);
+  count_chunks_kernel<<<dim3((unsigned)ceil_div(n_chunks, kCountWarps), n_pairs), kCountWarps * 32, 0,
+                        st>>>(kept, words_per_pair, n_chunks, chunk_rows);
   {
     const int64_t tiles = ceil_div(n_cw, kScanTile);
     tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(chunk_rows, n_cw, ctsum);
@@ -1882,8 +1990,9 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
                       pair_off + n_pairs, out_cap};
     const int64_t batch = out_cap < kPwCellsPerLaunch ? out_cap : kPwCellsPerLaunch;
     for (int64_t first = 0; first < out_cap; first += kPwCellsPerLaunch, launches += 2) {
-      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)batch), kPwRootThreads, 0,
-                        st>>>(g, pcs, thr_unique, h, scores, cl, first, pwplan, pwvals);
+      pw_roots_kernel<<<dim3(kPwPlanRoots / kPwRootThreads, (unsigned)min(batch, kPwRootGridY)),
+                        kPwRootThreads, 0, st>>>(g, pcs, thr_unique, h, scores, cl, first, batch,
+                                                 pwplan, pwvals);
       pw_combine_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, st>>>(cl, first, pwplan, pwvals,
                                                                         (double)n, out_fid);
     }
