@@ -228,7 +228,10 @@ __device__ void block_reduce_store(Best mine, Best* out) {
 }
 
 // grid: (row blocks, points)
-__global__ void __launch_bounds__(kPlanThreads)
+#ifndef HADIS_K5_MINB
+#define HADIS_K5_MINB 4      // 4 CTAs/SM (64 registers): c5 2.97 -> 1.92 ms; 1 or 2: 101-108 registers
+#endif
+__global__ void __launch_bounds__(kPlanThreads, HADIS_K5_MINB)
 solve_rows_kernel(PlanIn in, int fallback, const int32_t* __restrict__ need_fb,
                   Best* __restrict__ partial) {
   const int p = blockIdx.y;
