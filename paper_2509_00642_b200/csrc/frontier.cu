@@ -1092,7 +1092,7 @@ constexpr int kDecThreads = 256;
 constexpr int kDecChunk = 1024;
 constexpr int kDecWin = 3072;
 
-__global__ void __launch_bounds__(kDecThreads)
+__global__ void __launch_bounds__(kDecThreads)   // 6 / 8 CTAs per SM forced: same / worse
 decide_kernel(Grid g, const PairConst* __restrict__ pcs,
               const unsigned long long* __restrict__ counters_ro, int64_t cap,
               const unsigned long long* __restrict__ boff, const uint32_t* __restrict__ bcnt,
