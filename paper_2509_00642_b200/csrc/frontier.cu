@@ -1844,9 +1844,10 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   int launches = 31;   // fixed kernels below; batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_classes_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)((size_t)n_unique * 12)));
+  if ((size_t)n_unique * 12 > 30 * 1024)   // opt in only near the 48 KB default (~17 KB static)
+    HADIS_CUDA_TRY(cudaFuncSetAttribute(row_classes_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)((size_t)n_unique * 12)));
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 12, st>>>(pre_cnt, n_unique, n_unique + 1,
                                                             first_pos, pk, row_rep, row_start,
                                                             sorted);
