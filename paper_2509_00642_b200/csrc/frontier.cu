@@ -1596,8 +1596,12 @@ struct Rows {
 __global__ void __launch_bounds__(kEmitWords, 6)
 emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __restrict__ kept_bm,
                  int64_t words_per_pair, int n_chunks,
-                 const unsigned long long* __restrict__ chunk_off, int64_t out_cap, Rows out) {
+                 const unsigned long long* __restrict__ chunk_off, int64_t out_cap, Rows out,
+                 const unsigned long long* __restrict__ counters, int exact_fid) {
   __shared__ uint32_t s_cell[kEmitWords * 32];
+  // the row -> cell map is read only by the exact-fidelity passes: skip it when
+  // none will run (no exact requests, exact_fid off: 45 MB of stores at c4)
+  const bool keep_cell = exact_fid || counters[2] != 0;
   const int p = blockIdx.y, ch = blockIdx.x;
   const int64_t wi = (int64_t)ch * kEmitWords + threadIdx.x;
   const uint32_t word = wi < words_per_pair ? kept_bm[(int64_t)p * words_per_pair + wi] : 0u;
@@ -1620,11 +1624,11 @@ emit_rows_kernel(Grid g, const PairConst* __restrict__ pcs, const uint32_t* __re
     if (c >= cells || r >= out_cap) continue;
     const int k = (int)((uint32_t)c / (uint32_t)g.U), t = (int)((uint32_t)c - (uint32_t)k * g.U);
     const CellVal v = eval_cell(g, pc, k, t);
-    out.pair[r] = p;
+    if (keep_cell || out.n_light == nullptr) out.pair[r] = p;   // compact: workspace only
     out.theta_pos[r] = g.first_pos[k];
     out.tau_pos[r] = g.first_pos[t];
     out.fid[r] = v.fid;
-    out.cell[r] = (uint32_t)c;
+    if (keep_cell) out.cell[r] = (uint32_t)c;
     if (out.n_light != nullptr) {                  // compact rows (uniform branch)
       out.n_light[r] = v.n_keep_light;
       out.n_heavy[r] = v.n_heavy;
@@ -1983,7 +1987,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   Rows out{out_pair,    out_theta_pos, out_tau_pos, out_r_light, out_r_heavy,
            out_fid,     out_lat,       row_cell,    out_n_light, out_n_heavy};
   emit_rows_kernel<<<dim3(n_chunks, n_pairs), kEmitWords, 0, st>>>(
-      g, pcs, kept, words_per_pair, n_chunks, chunk_off, out_cap, out);
+      g, pcs, kept, words_per_pair, n_chunks, chunk_off, out_cap, out, counters, exact_fid);
   if (exact_fid) {
     // every emitted row; out_cap bounds the batches launched (rows beyond the
     // device row count exit immediately)
