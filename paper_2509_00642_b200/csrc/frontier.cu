@@ -1074,7 +1074,8 @@ __global__ void group_cands_kernel(Grid g, const PairConst* __restrict__ pcs,
     atomicMin(&fmin[key], (unsigned long long)order_key(cd.fid));
     cd.lat = div_n(cd.lat, dn, g.rn);     // the list holds raw numerators
     cd.fid = div_n(cd.fid, dn, g.rn);
-    grp.c[(int64_t)boff[key] + atomicAdd(&bcur[key], 1u)] = cd;
+    // in-bucket slot: the bucket's count, consumed downwards (no cursor array to zero)
+    grp.c[(int64_t)boff[key] + atomicSub(&bcur[key], 1u) - 1u] = cd;
   }
 }
 
@@ -1689,7 +1690,7 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, bcur, boff, grp, lst, kept, reqbm, un[3], req[3],
+  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, boff, grp, lst, kept, reqbm, un[3], req[3],
       counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell,
       row_pair, rsort[5], rsort_bytes, total;
 };
@@ -1716,7 +1717,6 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.cpre = take(8 * (pb >> kCoarseShift));
   L.ctmin = take(8 * (ceil_div(nbuckets >> kCoarseShift, 4096) * n_pairs + 1));
   L.bcnt = take(4 * pb);
-  L.bcur = take(4 * pb);
   L.boff = take(8 * (pb + 1));
   L.grp = take(sizeof(Cand) * cap);
   L.lst = take(sizeof(ListCand) * cap);
@@ -1808,7 +1808,6 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   double* cpre = (double*)P(L.cpre);
   unsigned long long* ctmin = (unsigned long long*)P(L.ctmin);
   uint32_t* bcnt = (uint32_t*)P(L.bcnt);
-  uint32_t* bcur = (uint32_t*)P(L.bcur);
   unsigned long long* boff = (unsigned long long*)P(L.boff);
   Cands grp{(Cand*)P(L.grp)};
   ListCand* lst = (ListCand*)P(L.lst);
@@ -1837,7 +1836,6 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   HADIS_CUDA_TRY(cudaMemsetAsync(bmin, 0xff, 8 * pb, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(cmin, 0xff, 8 * (pb >> kCoarseShift), st));
   HADIS_CUDA_TRY(cudaMemsetAsync(bcnt, 0, 4 * pb, st));
-  HADIS_CUDA_TRY(cudaMemsetAsync(bcur, 0, 4 * pb, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(kept, 0, 4 * words_per_pair * n_pairs, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(reqbm, 0, 4 * words_per_pair * n_pairs, st));
   HADIS_CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * 8, st));
@@ -1921,7 +1919,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   }
   // grid sizes of the two grid-stride passes measured at c4 (4 / 32 CTAs per SM)
   group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, lst, counters + 5, cand_cap, nb, (double)n, boff,
-                                                  bcur, grp, bmin);
+                                                  bcnt, grp, bmin);
   prefix(bmin, nb, tmin, gpre);                    // exact fine G for decide
   HADIS_LAUNCH_CHECK();
   decide_kernel<<<kNumSMs * 32, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
