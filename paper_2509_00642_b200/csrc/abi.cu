@@ -4,6 +4,9 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 static thread_local char g_last_cuda_error[256] = "";
 static std::atomic<long long> g_launches{0};
@@ -14,6 +17,20 @@ extern "C" int64_t hadis_kernel_launches(void) { return g_launches.load(); }
 
 void hadis_set_cuda_error(cudaError_t e) {
   std::strncpy(g_last_cuda_error, cudaGetErrorString(e), sizeof(g_last_cuda_error) - 1);
+}
+
+cudaError_t hadis_ensure_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& g = granted[{dev, func}];
+  if (bytes <= g) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) g = bytes;
+  return e;
 }
 
 extern "C" int hadis_abi_version(void) { return HADIS_ABI_VERSION; }

@@ -20,6 +20,10 @@
 #define HADIS_LAUNCH_CHECK() HADIS_CUDA_TRY(cudaGetLastError())
 
 void hadis_set_cuda_error(cudaError_t e);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `func` needs more
+// than it was last granted on the current device: the call can cost
+// milliseconds of host time, and eager pipelines launch ~40 kernels per build.
+cudaError_t hadis_ensure_smem(const void* func, size_t bytes);
 void hadis_count_launches(int k);  // bookkeeping for hadis_kernel_launches()
 
 namespace hadis {

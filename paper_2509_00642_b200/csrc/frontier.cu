@@ -1847,9 +1847,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   if ((size_t)n_unique * 12 > 30 * 1024)   // opt in only near the 48 KB default (~17 KB static)
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(row_classes_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)((size_t)n_unique * 12)));
+    HADIS_CUDA_TRY(hadis_ensure_smem((const void*)row_classes_kernel, (size_t)((size_t)n_unique * 12)));
   row_classes_kernel<<<1, 1024, (size_t)n_unique * 12, st>>>(pre_cnt, n_unique, n_unique + 1,
                                                             first_pos, pk, row_rep, row_start,
                                                             sorted);
@@ -1859,10 +1857,8 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   group_kernel<<<1, 32, 0, st>>>(pair_slot, n_pairs, group_p0, n_groups, counters, kMaxGroup);
   const size_t rsm = sizeof(RowSmem);
   const size_t fsm = rsm + (size_t)kRowWarps * kMaxGroup * 32;   // + per-window pass masks
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_min_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(filter_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)bucket_min_kernel, (size_t)rsm));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)filter_kernel, (size_t)fsm));
 #ifndef HADIS_F1_STRIDE
 #define HADIS_F1_STRIDE 4      // F1 over every 4th theta-row only
 #endif
@@ -1927,8 +1923,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
   // always opt in: the kernel's static shared memory counts against the 48 KB
   // default too (U = 2047 needs 49128 B dynamic + the static block-scan arrays)
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(nobypass_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)nobypass_kernel, (size_t)row_smem));
   nobypass_kernel<<<n_pairs, kRowThreads, row_smem, st>>>(g, pcs, kept, un, exact_cap, reqbm,
                                                           req_pair, req_cell, exact_cap, counters);
   HADIS_LAUNCH_CHECK();

@@ -211,8 +211,7 @@ extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, 
   const size_t smem_priv = (size_t)bins * 12 + 8 + (size_t)n_unique * 8;
   const int64_t blocks_needed = ceil_div(n, kHistThreads);
   if (smem_priv <= 160 * 1024) {
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_smem_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HADIS_CUDA_TRY(hadis_ensure_smem((const void*)bin_hist_smem_kernel, (size_t)200 * 1024));
     const int per_sm = smem_priv <= 48 * 1024 ? 4 : (smem_priv <= 100 * 1024 ? 2 : 1);
     int64_t grid = (int64_t)kNumSMs * per_sm;
     if (grid > blocks_needed) grid = blocks_needed;
@@ -222,8 +221,7 @@ extern "C" int hadis_bin_hist(const double* h, const double* scores, int64_t n, 
   } else {
     const size_t smem = n_unique <= kMaxSmemThr ? (size_t)n_unique * 8 : 0;
     // opt in unconditionally: static shared memory counts against the 48 KB default
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(bin_hist_global_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HADIS_CUDA_TRY(hadis_ensure_smem((const void*)bin_hist_global_kernel, (size_t)smem));
     int64_t grid = (int64_t)kNumSMs * 4;
     if (grid > blocks_needed) grid = blocks_needed;
     bin_hist_global_kernel<<<(unsigned)grid, kHistThreads, smem, st>>>(

@@ -1110,8 +1110,7 @@ extern "C" int hadis_records_plan(const double* h, int64_t n, const double* thr_
   bucket_setup_kernel<<<(unsigned)ceil_div(kGuide + 2, 256), 256, 0, st>>>(thr_unique, n_unique, rp);
   HADIS_LAUNCH_CHECK();
   const size_t csmem = (size_t)4 * (kMaxBins + kGuide + 2) + (size_t)8 * (n_unique + 2);
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_count_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)bucket_count_kernel, (size_t)csmem));
   int64_t cgrid = ceil_div(n, 2 * kCountThreads * 8);
   if (cgrid > kNumSMs * 2) cgrid = kNumSMs * 2;
   bucket_count_kernel<<<(unsigned)cgrid, kCountThreads, csmem, st>>>(h, n, thr_unique, n_unique, rp);
@@ -1145,8 +1144,7 @@ extern "C" int hadis_records_scatter(const double* h, const double* scores, int6
   if (vec && tsmem <= kTmaSmemMax && !(legacy && legacy[0] == '1')) {
     // aligned record arrays: the TMA-fed scatter over the plan's record ranges
     // (binning mode read on the device)
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(bucket_scatter_tma_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+    HADIS_CUDA_TRY(hadis_ensure_smem((const void*)bucket_scatter_tma_kernel, (size_t)tsmem));
     int64_t tgrid = ceil_div(n, kTmaTile);
     if (tgrid > kNumSMs) tgrid = kNumSMs;
     bucket_scatter_tma_kernel<<<(unsigned)tgrid, kTmaThreads, tsmem, st>>>(
@@ -1157,7 +1155,7 @@ extern "C" int hadis_records_scatter(const double* h, const double* scores, int6
   }
   const size_t ssmem = scatter_smem(n_unique);
   auto kern = vec ? bucket_scatter_kernel<true> : bucket_scatter_kernel<false>;
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)kern, (size_t)ssmem));
   kern<<<(unsigned)sgrid, kBkThreads, ssmem, st>>>(h, scores, n, n_light, thr_unique, n_unique,
                                                    hscale, rp, hfix_rows, bs_rows);
   HADIS_LAUNCH_CHECK();
@@ -1204,8 +1202,7 @@ extern "C" int hadis_bin_hist_rows(const uint64_t* hfix_rows, const uint16_t* bs
   const int B1s = (n_unique + 1) | 1;
   const size_t ksmem = (size_t)kQuad * 4 * B1s * 4;
   // opt in unconditionally: static shared memory counts against the 48 KB default
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(row_hist_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)row_hist_kernel, (size_t)ksmem));
   const dim3 grid((unsigned)n_quads(n_light), (unsigned)max_items);
   row_hist_kernel<<<grid, kK1Threads, ksmem, st>>>(hfix_rows, bs_rows, n, n_unique, n_light, rp,
                                                   hist_cnt, (unsigned long long*)hist_hsum,

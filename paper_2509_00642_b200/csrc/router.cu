@@ -131,8 +131,7 @@ extern "C" int hadis_tune_weights(const double* features, const uint8_t* labels,
   int npow = 1;
   while (npow < n) npow <<= 1;
   const size_t smem = (size_t)npow * 8 + (size_t)(npow + 1) * 4 + (size_t)npow * 4 + npow + 16;
-  HADIS_CUDA_TRY(cudaFuncSetAttribute(tune_weights_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HADIS_CUDA_TRY(hadis_ensure_smem((const void*)tune_weights_kernel, (size_t)smem));
   const int grid = n_vectors < kNumSMs * 4 ? n_vectors : kNumSMs * 4;
   tune_weights_kernel<<<grid, kTwThreads, smem, (cudaStream_t)stream>>>(
       features, labels, n, n_features, weights, n_vectors, n_pos, out_acc, out_threshold);

@@ -494,9 +494,7 @@ extern "C" size_t hadis_text_workspace_bytes(int64_t n) {
 static int text_smem_optin() {
   static int done = 0;
   if (!done) {
-    HADIS_CUDA_TRY(cudaFuncSetAttribute(text_records_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(sizeof(hadis_lexicon))));
+    HADIS_CUDA_TRY(hadis_ensure_smem((const void*)text_records_kernel, (size_t)int(sizeof(hadis_lexicon))));
     done = 1;
   }
   return HADIS_OK;
