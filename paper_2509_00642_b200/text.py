@@ -234,6 +234,12 @@ def digest_part(part) -> bytes:
 
 def pack_texts(texts):
     """UTF-8 byte buffer + int64 offsets[n + 1] (host numpy)."""
+    joined = "".join(texts)
+    if joined.isascii():                 # byte lengths = character lengths: one encode
+        offs = np.zeros(len(texts) + 1, dtype=np.int64)
+        np.cumsum(np.fromiter(map(len, texts), dtype=np.int64, count=len(texts)), out=offs[1:])
+        blob = np.frombuffer(bytearray(joined.encode("ascii") or b"\0"), dtype=np.uint8)
+        return blob, offs
     enc = [t.encode("utf-8") for t in texts]
     offs = np.zeros(len(enc) + 1, dtype=np.int64)
     np.cumsum(np.fromiter(map(len, enc), dtype=np.int64, count=len(enc)), out=offs[1:])

@@ -5,6 +5,8 @@ import ctypes
 import os
 import struct
 
+import numpy as np
+
 import pytest
 
 from oracle import text as ot
@@ -99,3 +101,15 @@ def test_prompts_hash_and_keys_are_the_reference_values():
         texts = [x if isinstance(x, str) else x[0] for x in texts]
         assert prompts_hash(texts) == gold["misc"]["prompts_hash"][name]
         assert prompts_hash(list(reversed(texts))) == gold["misc"]["prompts_hash"][name]
+
+
+@pytest.mark.parametrize("texts", [["abc", "", "d e"], ["Émile x", "y", ""], [], [""],
+                                   ["plain ascii", "naïve café", "日本"]])
+def test_pack_texts_layout(texts):
+    """pack_texts (ASCII fast path and the general UTF-8 path): blob = the
+    concatenated UTF-8 bytes, offsets = their running byte lengths."""
+    from paper_2509_00642_b200.text import pack_texts
+    blob, offs = pack_texts(texts)
+    enc = [t.encode("utf-8") for t in texts]
+    assert offs.tolist() == [0] + list(np.cumsum([len(e) for e in enc]).tolist())
+    assert bytes(blob[:offs[-1]]) == b"".join(enc)
