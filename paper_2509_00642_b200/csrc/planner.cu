@@ -169,6 +169,67 @@ __device__ Best eval_row(const PlanIn& in, int p, int r) {
   return best;
 }
 
+// eval_row with the batch loops unrolled for n_batch <= kNB: the heavy model's
+// per-batch worker counts stay in registers (the generic version keeps them in
+// a local-memory array), counts clamped to W + 1 (only "> W" is ever asked)
+template <int kNB>
+__device__ Best eval_row_small(const PlanIn& in, int p, int r) {
+  Best best;
+  best.row = -1;
+  const RowShape s = row_shape(in, r);
+  const double lamv = in.lam[p];
+  const int W = in.workers[p];
+  const double limit = __dadd_rn(in.t_slo[p], kSlack);
+  const int nb = in.n_batch;
+  const int nl = s.al ? nb : 1;
+  const int nh = s.ah ? nb : 1;
+  const double* Q = in.queues + (int64_t)p * in.n_models;
+  const double rate_l = __dmul_rn(lamv, s.sl);
+  const double dl = drain(Q[s.ml], rate_l, in.alpha);
+  double rate_h = 0.0, dh = 0.0;
+  if (!s.single) {
+    rate_h = __dmul_rn(lamv, s.sh);
+    dh = drain(Q[s.mh], rate_h, in.alpha);
+  }
+  auto clampw = [&](int64_t x) { return (int)(x > (int64_t)W ? (int64_t)W + 1 : x); };
+  int xh_b[kNB];
+#pragma unroll
+  for (int ih = 0; ih < kNB; ++ih)
+    xh_b[ih] = (ih < nh && s.ah) ? clampw(min_workers(rate_h, in.mu[s.mh * nb + ih])) : 0;
+  double best_total = 0.0, best_path = 0.0;
+#pragma unroll 1
+  for (int il = 0; il < nl; ++il) {
+    const int xl = s.al ? clampw(min_workers(rate_l, in.mu[s.ml * nb + il])) : 0;
+    if (xl > W) continue;                             // every combo of this il is over budget
+    const double pl = __dadd_rn(0.0, __dadd_rn(in.lat[s.ml * nb + il], dl));
+#pragma unroll
+    for (int ih = 0; ih < kNB; ++ih) {
+      if (ih >= nh) break;
+      const int total = xl + xh_b[ih];
+      if (total > W) continue;
+      const double path = s.single ? pl : __dadd_rn(pl, __dadd_rn(in.lat[s.mh * nb + ih], dh));
+      if (path > limit) continue;
+      const double tot = (double)total;
+      if (best.row < 0 || tot < best_total || (tot == best_total && path < best_path)) {
+        best.row = r;
+        best_total = tot;
+        best_path = path;
+        best.xl = xl;
+        best.xh = xh_b[ih];
+        best.bl = il;
+        best.bh = ih;
+      }
+    }
+  }
+  if (best.row >= 0) {
+    best.k0 = in.row_fid[r];
+    best.k1 = best_total;
+    best.k2 = best_path;
+    best.path = best_path;
+  }
+  return best;
+}
+
 // fallback_plan candidate of one row (planner.py:179-208)
 __device__ Best fallback_row(const PlanIn& in, int p, int r) {
   Best best;
@@ -240,7 +301,8 @@ solve_rows_kernel(PlanIn in, int fallback, const int32_t* __restrict__ need_fb,
   mine.row = -1;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < in.n_rows;
        r += gridDim.x * blockDim.x) {
-    const Best c = fallback ? fallback_row(in, p, r) : eval_row(in, p, r);
+    const Best c = fallback ? fallback_row(in, p, r)
+                            : (in.n_batch <= 8 ? eval_row_small<8>(in, p, r) : eval_row(in, p, r));
     if (better(c, mine)) mine = c;
   }
   block_reduce_store(mine, partial + (int64_t)p * gridDim.x + blockIdx.x);
