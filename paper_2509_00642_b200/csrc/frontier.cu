@@ -33,6 +33,8 @@
 #include <cmath>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "common.cuh"
 #include "pairwise.cuh"
@@ -1687,12 +1689,39 @@ fid_exact_kernel(const double* __restrict__ h, const double* __restrict__ scores
   }
 }
 
+// ------------------------------------------------- single-pass scan (CUB)
+// The bucket offsets (exclusive sum of the per-bucket candidate counts) run as
+// a CUB decoupled-look-back scan: one read and one write per bucket (the
+// three-launch tile scan read twice: c4 53 -> 32 us).  The per-pair prefix
+// minima stay on the tile kernels: a CUB segmented-min scan over (min, head)
+// pairs measured 5x slower (non-word tile state, per-element modulo).
+
+struct CountIn {        // bucket counts widened to 64 bits, 0 past the end
+  const uint32_t* cnt;
+  int64_t n;
+  __host__ __device__ unsigned long long operator()(int64_t i) const {
+    return i < n ? (unsigned long long)cnt[i] : 0ull;
+  }
+};
+
+static cudaError_t count_offsets(void* temp, size_t& temp_bytes, const uint32_t* cnt, int64_t n,
+                                 unsigned long long* off, cudaStream_t st) {
+  auto in = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), CountIn{cnt, n});
+  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, off, n + 1, st);   // off[n] = total
+}
+
+static size_t scan_temp_bytes(int64_t pb) {
+  size_t c = 0;
+  count_offsets(nullptr, c, nullptr, pb, nullptr, 0);
+  return c;
+}
+
 // ------------------------------------------------------------ workspace
 
 struct Layout {
   size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, boff, grp, lst, kept, reqbm, un[3], req[3],
       counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell,
-      row_pair, rsort[5], rsort_bytes, total;
+      row_pair, scan_temp, scan_temp_bytes, rsort[5], rsort_bytes, total;
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1737,6 +1766,8 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
   L.row_pair = take(4 * out_cap);                  // compact outputs: pair ids of the rows
+  L.scan_temp_bytes = scan_temp_bytes(pb);
+  L.scan_temp = take(L.scan_temp_bytes ? L.scan_temp_bytes : 1);
   if (ecap > kSortMax) {                           // CUB request sort (see pack_requests_kernel)
     L.rsort[0] = take(8 * ecap); L.rsort[1] = take(8 * ecap);     // keys in / out
     L.rsort[2] = take(8 * ecap); L.rsort[3] = take(8 * ecap);     // fid in / out
@@ -1843,7 +1874,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted,
          1.0 / (double)n};
-  int launches = 31;   // fixed kernels below; batched emulation adds 2 per batch
+  int launches = 30;   // fixed kernels below (the CUB scan is 2); batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   if ((size_t)n_unique * 12 > 30 * 1024)   // opt in only near the 48 KB default (~17 KB static)
@@ -1883,10 +1914,8 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   filter_kernel<<<row_grid, kRowWarps * 32, fsm, st>>>(g, pcs, group_p0, n_groups, cpre, bcnt, lst,
                                                      cand_cap, counters + 5);
   {
-    const int64_t tiles = ceil_div(pb, kScanTile);
-    tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum);
-    tile_offsets_kernel<<<1, kScanThreads, 0, st>>>(tsum, tiles, boff + pb);
-    tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(bcnt, pb, tsum, boff);
+    size_t tb = L.scan_temp_bytes;
+    HADIS_CUDA_TRY(count_offsets(P(L.scan_temp), tb, bcnt, pb, boff, st));
   }
   candidates_total_kernel<<<1, 1, 0, st>>>(boff + pb, counters);
   if (getenv("HADIS_DEBUG_BUCKETS")) {             // measurement aid: fine-bucket occupancy
