@@ -1710,9 +1710,9 @@ static cudaError_t count_offsets(void* temp, size_t& temp_bytes, const uint32_t*
   return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, off, n + 1, st);   // off[n] = total
 }
 
-static size_t scan_temp_bytes(int64_t pb) {
+static size_t scan_temp_bytes(int64_t items) {   // enough for any scan of <= items
   size_t c = 0;
-  count_offsets(nullptr, c, nullptr, pb, nullptr, 0);
+  count_offsets(nullptr, c, nullptr, items, nullptr, 0);
   return c;
 }
 
@@ -1766,7 +1766,7 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
   L.row_pair = take(4 * out_cap);                  // compact outputs: pair ids of the rows
-  L.scan_temp_bytes = scan_temp_bytes(pb);
+  L.scan_temp_bytes = scan_temp_bytes(std::max<int64_t>(pb, n_cw));
   L.scan_temp = take(L.scan_temp_bytes ? L.scan_temp_bytes : 1);
   if (ecap > kSortMax) {                           // CUB request sort (see pack_requests_kernel)
     L.rsort[0] = take(8 * ecap); L.rsort[1] = take(8 * ecap);     // keys in / out
@@ -1874,7 +1874,7 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   Grid g{pre_cnt, pre_hsum, n, n_unique, n_unique + 1, ldexp(1.0, -hfix_shift), nb,
          n_thresholds, first_pos, words_per_pair * 32, pk, row_rep, row_start, sorted,
          1.0 / (double)n};
-  int launches = 30;   // fixed kernels below (the CUB scan is 2); batched emulation adds 2 per batch
+  int launches = 29;   // fixed kernels below (a CUB scan is 2); batched emulation adds 2 per batch
   pair_const_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       n_pairs, pair_slot, pair_params, n, hfix_shift, nb, pcs);
   if ((size_t)n_unique * 12 > 30 * 1024)   // opt in only near the 48 KB default (~17 KB static)
@@ -1997,11 +1997,9 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   const int64_t n_cw = (int64_t)n_chunks * n_pairs;
   count_chunks_kernel<<<dim3((unsigned)ceil_div(n_chunks, kCountWarps), n_pairs), kCountWarps * 32, 0,
                         st>>>(kept, words_per_pair, n_chunks, chunk_rows);
-  {
-    const int64_t tiles = ceil_div(n_cw, kScanTile);
-    tile_sum_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(chunk_rows, n_cw, ctsum);
-    tile_offsets_kernel<<<1, kScanThreads, 0, st>>>(ctsum, tiles, chunk_off + n_cw);
-    tile_scan_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(chunk_rows, n_cw, ctsum, chunk_off);
+  {                                                // chunk row offsets (same CUB scan)
+    size_t tb = L.scan_temp_bytes;
+    HADIS_CUDA_TRY(count_offsets(P(L.scan_temp), tb, chunk_rows, n_cw, chunk_off, st));
   }
   pair_offsets_kernel<<<(unsigned)ceil_div(n_pairs, 128), 128, 0, st>>>(
       chunk_off, n_chunks, n_pairs, pair_off, stats, out_cap, counters);
