@@ -775,9 +775,8 @@ prefix_apply_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
 
 // ---------------------------------------------- F4: offsets (exclusive scan)
 
-// Device-wide exclusive scan of n u32 counts into u64 offsets (out[n] = total):
-// tile sums -> one-CTA scan of the tile sums -> per-tile scan with carry-in.
-constexpr int kScanTile = 4096;   // 1024 threads x 4 elements
+// (the bucket and chunk offsets are CUB scans, see count_offsets; the block
+// scan below serves emit)
 
 __device__ __forceinline__ unsigned long long block_exclusive_sum(unsigned long long v,
                                                                   unsigned long long* total) {
@@ -808,47 +807,6 @@ __device__ __forceinline__ unsigned long long block_exclusive_sum(unsigned long 
   return before;
 }
 
-__global__ void __launch_bounds__(kScanThreads)
-tile_sum_kernel(const uint32_t* __restrict__ in, int64_t n, unsigned long long* __restrict__ sums) {
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
-  unsigned long long v = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) v += base + j < n ? in[base + j] : 0u;
-  unsigned long long total;
-  block_exclusive_sum(v, &total);
-  if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(kScanThreads)
-tile_offsets_kernel(unsigned long long* __restrict__ sums, int64_t tiles,
-                    unsigned long long* __restrict__ grand_total) {
-  unsigned long long carry = 0;
-  for (int64_t c0 = 0; c0 < tiles; c0 += blockDim.x) {
-    const int64_t i = c0 + threadIdx.x;
-    const unsigned long long v = i < tiles ? sums[i] : 0ull;
-    unsigned long long total;
-    const unsigned long long ex = block_exclusive_sum(v, &total);
-    if (i < tiles) sums[i] = carry + ex;
-    carry += total;
-  }
-  if (threadIdx.x == 0) *grand_total = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(const uint32_t* __restrict__ in, int64_t n,
-                 const unsigned long long* __restrict__ sums, unsigned long long* __restrict__ out) {
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
-  uint32_t v[4];
-  unsigned long long local = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) { v[j] = base + j < n ? in[base + j] : 0u; local += v[j]; }
-  unsigned long long run = sums[blockIdx.x] + block_exclusive_sum(local, nullptr);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (base + j < n) out[base + j] = run;
-    run += v[j];
-  }
-}
 
 // --------------------------------------------------------------- F6: decide
 
@@ -1719,8 +1677,8 @@ static size_t scan_temp_bytes(int64_t items) {   // enough for any scan of <= it
 // ------------------------------------------------------------ workspace
 
 struct Layout {
-  size_t pcs, pk, row_rep, row_start, sorted, tsum, bmin, gpre, cmin, cpre, ctmin, bcnt, boff, grp, lst, kept, reqbm, un[3], req[3],
-      counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, ctsum, pair_off, row_cell,
+  size_t pcs, pk, row_rep, row_start, sorted, bmin, gpre, cmin, cpre, ctmin, bcnt, boff, grp, lst, kept, reqbm, un[3], req[3],
+      counters, groups, tmin, pwplan, pwvals, pair_rows, chunk_off, pair_off, row_cell,
       row_pair, scan_temp, scan_temp_bytes, rsort[5], rsort_bytes, total;
 };
 
@@ -1739,7 +1697,6 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   L.row_rep = take(sizeof(int32_t) * U);
   L.row_start = take(U);
   L.sorted = take(4);
-  L.tsum = take(8 * (ceil_div(pb, 4096) + 1));
   L.bmin = take(8 * pb);
   L.gpre = take(8 * pb);
   L.cmin = take(8 * (pb >> kCoarseShift));
@@ -1762,7 +1719,6 @@ static Layout make_layout(int n_pairs, int U, int nbuckets, int64_t cap, int64_t
   const int64_t n_cw = ceil_div((cells + 31) / 32, kEmitWords) * n_pairs;   // emit chunks
   L.pair_rows = take(4 * n_cw);
   L.chunk_off = take(8 * (n_cw + 1));
-  L.ctsum = take(8 * (ceil_div(n_cw, 4096) + 1));
   L.pair_off = take(8 * (n_pairs + 1));
   L.row_cell = take(4 * out_cap);
   L.row_pair = take(4 * out_cap);                  // compact outputs: pair ids of the rows
@@ -1832,7 +1788,6 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   int32_t* row_rep = (int32_t*)P(L.row_rep);
   uint8_t* row_start = (uint8_t*)P(L.row_start);
   int32_t* sorted = (int32_t*)P(L.sorted);
-  unsigned long long* tsum = (unsigned long long*)P(L.tsum);
   unsigned long long* bmin = (unsigned long long*)P(L.bmin);
   double* gpre = (double*)P(L.gpre);
   unsigned long long* cmin = (unsigned long long*)P(L.cmin);
@@ -1856,7 +1811,6 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   double* pwvals = (double*)P(L.pwvals);
   uint32_t* chunk_rows = (uint32_t*)P(L.pair_rows);
   unsigned long long* chunk_off = (unsigned long long*)P(L.chunk_off);
-  unsigned long long* ctsum = (unsigned long long*)P(L.ctsum);
   unsigned long long* pair_off = (unsigned long long*)P(L.pair_off);
   uint32_t* row_cell = (uint32_t*)P(L.row_cell);
   int32_t* row_pair = (int32_t*)P(L.row_pair);
