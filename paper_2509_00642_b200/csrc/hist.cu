@@ -10,6 +10,8 @@
 // hardness sums follow from 2-D prefix sums of an (U+1) x (U+1) histogram per
 // light model.  Integer accumulation (counts u32, hardness in fixed point
 // 2^-shift as u64) is exact and order independent, hence deterministic.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace hadis {
@@ -119,12 +121,26 @@ __global__ void scan_rows_kernel(uint32_t* __restrict__ cnt, unsigned long long*
   }
 }
 
-// K2b: inclusive prefix along bh.  CTA = (32-column tile, light slot); each
-// of the 16 warps takes a contiguous band of rows (lanes = columns, so every
+// K2b: inclusive prefix along bh.  Task = (32-column tile, light slot); each
+// of the CTA's warps takes a contiguous band of rows (lanes = columns, so every
 // access is a coalesced 128/256-byte row segment), sums its band, the bands'
 // totals are scanned in shared memory, then each warp rewrites its band with
-// the carried-in prefix (the second read hits L2).
-constexpr int kColWarps = 16;
+// the carried-in prefix.  Persistent CTAs walk the tasks in order, so the
+// tables being scanned at any moment (CTAs x 1025 rows x 32 columns x 12 B,
+// ~58 MB at c4) stay L2-resident and the second read of a band hits L2: the
+// pass moves one read + one write of the tables from DRAM (a one-shot grid
+// of all 495 tasks keeps the whole 189 MB alive and re-reads it from DRAM).
+#ifndef HADIS_K2_WARPS
+#define HADIS_K2_WARPS 32
+#endif
+#ifndef HADIS_K2_UNROLL
+#define HADIS_K2_UNROLL 8
+#endif
+#ifndef HADIS_K2_CPS
+#define HADIS_K2_CPS 1
+#endif
+constexpr int kColWarps = HADIS_K2_WARPS;
+constexpr int kColU = HADIS_K2_UNROLL;
 
 __global__ void __launch_bounds__(kColWarps * 32)
 scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs, int n_light,
@@ -132,53 +148,58 @@ scan_cols_kernel(uint32_t* __restrict__ cnt, unsigned long long* __restrict__ hs
   __shared__ uint32_t s_c[kColWarps][32];
   __shared__ unsigned long long s_h[kColWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
-  const int64_t l = blockIdx.y;
+  const int tiles = (B1 + 31) / 32;
   const int band = (B1 + kColWarps - 1) / kColWarps;
-  const int k0 = warp * band, k1 = min(B1, k0 + band);
-  uint32_t* c = cnt + l * B1 * (int64_t)B1 + t;
-  unsigned long long* h = hs + l * B1 * (int64_t)B1 + t;
-  const bool col = t < B1;
-  uint32_t sc = 0;
-  unsigned long long sh = 0;
-  if (col) {
-    int k = k0;
-    for (; k + 4 <= k1; k += 4) {
-      uint32_t vc[4];
-      unsigned long long vh[4];
+  const int k0 = min(B1, warp * band), k1 = min(B1, k0 + band);
+  for (int task = blockIdx.x; task < tiles * n_light; task += gridDim.x) {
+    const int t = (task % tiles) * 32 + lane;
+    const int64_t l = task / tiles;
+    uint32_t* c = cnt + l * B1 * (int64_t)B1 + t;
+    unsigned long long* h = hs + l * B1 * (int64_t)B1 + t;
+    const bool col = t < B1;
+    uint32_t sc = 0;
+    unsigned long long sh = 0;
+    if (col) {
+      int k = k0;
+      for (; k + kColU <= k1; k += kColU) {
+        uint32_t vc[kColU];
+        unsigned long long vh[kColU];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
+        for (int j = 0; j < kColU; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) { sc += vc[j]; sh += vh[j]; }
+        for (int j = 0; j < kColU; ++j) { sc += vc[j]; sh += vh[j]; }
+      }
+      for (; k < k1; ++k) { sc += c[(int64_t)k * B1]; sh += h[(int64_t)k * B1]; }
     }
-    for (; k < k1; ++k) { sc += c[(int64_t)k * B1]; sh += h[(int64_t)k * B1]; }
-  }
-  s_c[warp][lane] = sc;
-  s_h[warp][lane] = sh;
-  __syncthreads();
-  uint32_t rc = 0;
-  unsigned long long rh = 0;
-  for (int w = 0; w < warp; ++w) { rc += s_c[w][lane]; rh += s_h[w][lane]; }
-  if (!col) return;
-  int k = k0;
-  for (; k + 4 <= k1; k += 4) {
-    uint32_t vc[4];
-    unsigned long long vh[4];
+    s_c[warp][lane] = sc;
+    s_h[warp][lane] = sh;
+    __syncthreads();
+    uint32_t rc = 0;
+    unsigned long long rh = 0;
+    for (int w = 0; w < warp; ++w) { rc += s_c[w][lane]; rh += s_h[w][lane]; }
+    if (col) {
+      int k = k0;
+      for (; k + kColU <= k1; k += kColU) {
+        uint32_t vc[kColU];
+        unsigned long long vh[kColU];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
+        for (int j = 0; j < kColU; ++j) { vc[j] = c[(int64_t)(k + j) * B1]; vh[j] = h[(int64_t)(k + j) * B1]; }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      rc += vc[j];
-      rh += vh[j];
-      c[(int64_t)(k + j) * B1] = rc;
-      h[(int64_t)(k + j) * B1] = rh;
+        for (int j = 0; j < kColU; ++j) {
+          rc += vc[j];
+          rh += vh[j];
+          c[(int64_t)(k + j) * B1] = rc;
+          h[(int64_t)(k + j) * B1] = rh;
+        }
+      }
+      for (; k < k1; ++k) {
+        rc += c[(int64_t)k * B1];
+        rh += h[(int64_t)k * B1];
+        c[(int64_t)k * B1] = rc;
+        h[(int64_t)k * B1] = rh;
+      }
     }
-  }
-  for (; k < k1; ++k) {
-    rc += c[(int64_t)k * B1];
-    rh += h[(int64_t)k * B1];
-    c[(int64_t)k * B1] = rc;
-    h[(int64_t)k * B1] = rh;
+    __syncthreads();                                 // s_c / s_h reused by the next task
   }
 }
 
@@ -242,7 +263,9 @@ extern "C" int hadis_hist_scan(uint32_t* hist_cnt, uint64_t* hist_hsum, int32_t 
   scan_rows_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, st>>>(
       hist_cnt, (unsigned long long*)hist_hsum, rows, B1, row_scanned);
   HADIS_LAUNCH_CHECK();
-  scan_cols_kernel<<<dim3((unsigned)ceil_div(B1, 32), (unsigned)n_light), kColWarps * 32, 0, st>>>(
+  const int64_t tasks = ceil_div((int64_t)B1, 32) * n_light;
+  const int64_t cgrid = std::min<int64_t>(tasks, (int64_t)kNumSMs * HADIS_K2_CPS);
+  scan_cols_kernel<<<(unsigned)cgrid, kColWarps * 32, 0, st>>>(
       hist_cnt, (unsigned long long*)hist_hsum, n_light, B1);
   HADIS_LAUNCH_CHECK();
   hadis_count_launches(2);
