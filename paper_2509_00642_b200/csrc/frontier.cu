@@ -1076,7 +1076,7 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     const double G = div_n(GS, dn, g.rn);
     const double lo = cd.fid - d2, hi = cd.fid + d2;
     bool kill = G < lo, close = G <= hi && !kill;
-    {                                                // kU mates' loads in flight per step
+    if (!kill) {                // (killed by G: no mates needed; kU mates' loads in flight per step)
       constexpr int kU = 8;                          // (c4: -12 us vs one at a time)
       int64_t j = s0;
       for (; j + kU <= s1; j += kU) {
@@ -1105,6 +1105,25 @@ decide_kernel(Grid g, const PairConst* __restrict__ pcs,
     decide_one(g, pcs[p], p, cd.cell, cd.lat, cd.fid, GS, grp, s0, s1, i, o,
                [&](int64_t q) { return make_double2(grp.c[q].lat, grp.c[q].fid); });
   }
+}
+
+// measurement aid (HADIS_DEBUG_BUCKETS): candidates the exact fine prefix G
+// alone kills (c4: 2.82M of 13.94M -- nearly every candidate that is not a row)
+__global__ void debug_kills_kernel(Grid g, const PairConst* __restrict__ pcs,
+                                   const unsigned long long* __restrict__ counters_ro, int64_t cap,
+                                   const double* __restrict__ gpre, Cands grp,
+                                   unsigned long long* __restrict__ out) {
+  if ((int64_t)counters_ro[0] > cap) return;
+  const int64_t m = (int64_t)counters_ro[0];
+  unsigned long long kills = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Cand cd = grp.c[i];
+    const int64_t key = (int64_t)cd.pair * g.nbuckets + cd.bucket;
+    const double G = div_n(gpre[key], (double)g.n, g.rn);
+    kills += G < cd.fid - pcs[cd.pair].delta2;
+  }
+  atomicAdd(out, kills);
 }
 
 // ------------------------------------------------- F7: no-bypass sub-frontier
@@ -1903,6 +1922,17 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
   HADIS_LAUNCH_CHECK();
   decide_kernel<<<kNumSMs * 32, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
+  if (getenv("HADIS_DEBUG_BUCKETS")) {
+    unsigned long long* dk = nullptr;
+    unsigned long long hk = 0;
+    cudaMalloc(&dk, 8);
+    cudaMemsetAsync(dk, 0, 8, st);
+    debug_kills_kernel<<<kNumSMs * 8, 256, 0, st>>>(g, pcs, counters, cand_cap, gpre, grp, dk);
+    cudaMemcpyAsync(&hk, dk, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(dk);
+    fprintf(stderr, "candidates killed by the fine prefix G alone: %llu\n", hk);
+  }
   const size_t row_smem = (size_t)n_unique * (8 + 8 + 4 + 4);
   // always opt in: the kernel's static shared memory counts against the 48 KB
   // default too (U = 2047 needs 49128 B dynamic + the static block-scan arrays)
