@@ -72,6 +72,10 @@ constexpr int kTmaTile = kTmaPer * kTmaConsumers;      // records per tile (max)
 constexpr int kTmaSlots = HADIS_TMA_SLOTS;
 constexpr int kTmaBar = 1;                             // named barrier id (consumers)
 static_assert(kTmaPer % kTmaChunkPer == 0 && kTmaChunkPer % 2 == 0, "pairs per chunk");
+#ifndef HADIS_B3_WOBATCH
+#define HADIS_B3_WOBATCH 2
+#endif
+constexpr int kTmaRowsPer = (kMaxBins + kTmaConsumers - 1) / kTmaConsumers;   // rows per consumer (max)
 
 // Row plan (the `row_plan` buffer shared by B0..B3 and K1), offsets in bytes.
 struct RowPlan {
@@ -397,17 +401,27 @@ __device__ __forceinline__ void scatter_tile(const double* __restrict__ h,
   __syncthreads();
   // 2. local exclusive offsets + one global reservation per non-empty row
   {
+    constexpr int kPer = (kMaxBins + kBkThreads - 1) / kBkThreads;
     const int per = (B1 + blockDim.x - 1) / blockDim.x;
     const int i0 = threadIdx.x * per, i1 = min(B1, i0 + per);
+    uint32_t cv[kPer], gv[kPer];              // counts first: the cursor atomics overlap
     int64_t tsum = 0;
-    for (int i = i0; i < i1; ++i) tsum += sm.cnt[i];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      cv[j] = i0 + j < i1 ? sm.cnt[i0 + j] : 0u;
+      tsum += cv[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) gv[j] = cv[j] ? atomicAdd(&rp.cursor[i0 + j], cv[j]) : 0u;
     int64_t total;
     int64_t run = block_excl_scan(tsum, sm.warp, &total);
-    for (int i = i0; i < i1; ++i) {
-      const uint32_t c = sm.cnt[i];
-      sm.gbase[i] = c ? atomicAdd(&rp.cursor[i], c) : 0u;
-      sm.cnt[i] = (uint32_t)run;          // now the local row offsets
-      run += c;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      if (i0 + j < i1) {
+        sm.gbase[i0 + j] = gv[j];
+        sm.cnt[i0 + j] = (uint32_t)run;   // now the local row offsets
+      }
+      run += cv[j];
     }
     if (threadIdx.x == 0) *sm.tile_n = (uint32_t)total;
   }
@@ -673,6 +687,36 @@ __device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* f
   // streaming while the previous array drains.
   uint2* wo_quad = nullptr;           // null: hfix
   int wo_tn = 0, wo_done = kTmaPer;
+#if HADIS_B3_WOBATCH > 1
+  // kWB items at a time: every shared-memory read of the batch is issued
+  // before its global stores (a generic store may alias shared memory for the
+  // compiler, which would otherwise order each item's reads after the
+  // previous item's store)
+  auto wo_items = [&](int upto) {
+    constexpr int kWB = HADIS_B3_WOBATCH;
+    while (wo_done < upto) {
+      uint32_t gg[kWB];
+      unsigned long long vv[kWB];
+      bool ok[kWB];
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        const int i = c + (wo_done + u) * kTmaConsumers;
+        ok[u] = wo_done + u < upto && i < wo_tn;
+        gg[u] = ok[u] ? sm.gpos[i] : 0u;
+        const int si = ok[u] ? (wo_quad ? (int)sm.sidx[i] : i) : 0;
+        vv[u] = sm.st[si];
+      }
+#pragma unroll
+      for (int u = 0; u < kWB; ++u) {
+        if (ok[u]) {
+          if (wo_quad) wo_quad[gg[u]] = reinterpret_cast<const uint2&>(vv[u]);
+          else hfix_rows[gg[u]] = vv[u];
+        }
+      }
+      wo_done = min(upto, wo_done + kWB);
+    }
+  };
+#else
   auto wo_items = [&](int upto) {
     for (; wo_done < upto; ++wo_done) {
       const int i = c + wo_done * kTmaConsumers;
@@ -683,6 +727,7 @@ __device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* f
       }
     }
   };
+#endif
   // rows owned by this consumer (contiguous segment: scan order)
   const int per = (B1 + kTmaConsumers - 1) / kTmaConsumers;
   const int i0 = min(B1, c * per), i1 = min(B1, i0 + per);
@@ -722,17 +767,28 @@ __device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* f
       wo_items((k + 1) * kTmaPer / kTmaChunks);
     }
     named_sync(kTmaBar, kTmaConsumers);
-    // S: local row offsets + one global reservation per non-empty row
+    // S: local row offsets + one global reservation per non-empty row (the
+    // consumer's row counts are read into registers first, so its cursor
+    // atomics are all in flight at once instead of one round trip per row)
     {
+      uint32_t cv[kTmaRowsPer], gv[kTmaRowsPer];
       int64_t tsum = 0;
-      for (int i = i0; i < i1; ++i) tsum += sm.co[i];
+#pragma unroll
+      for (int j = 0; j < kTmaRowsPer; ++j) {
+        cv[j] = i0 + j < i1 ? sm.co[i0 + j] : 0u;
+        tsum += cv[j];
+      }
+#pragma unroll
+      for (int j = 0; j < kTmaRowsPer; ++j) gv[j] = cv[j] ? atomicAdd(&rp.cursor[i0 + j], cv[j]) : 0u;
       int64_t total;
       uint32_t run = (uint32_t)consumer_excl_scan(tsum, s_warp, &total);
-      for (int i = i0; i < i1; ++i) {
-        const uint32_t cnt = sm.co[i];
-        sm.co[i] = run;
-        sm.gb[i] = cnt ? atomicAdd(&rp.cursor[i], cnt) : 0u;
-        run += cnt;
+#pragma unroll
+      for (int j = 0; j < kTmaRowsPer; ++j) {
+        if (i0 + j < i1) {
+          sm.co[i0 + j] = run;
+          sm.gb[i0 + j] = gv[j];
+        }
+        run += cv[j];
       }
     }
     named_sync(kTmaBar, kTmaConsumers);
