@@ -688,10 +688,10 @@ __device__ __forceinline__ void scatter_consumers(const TmaSmem& sm, uint64_t* f
   uint2* wo_quad = nullptr;           // null: hfix
   int wo_tn = 0, wo_done = kTmaPer;
 #if HADIS_B3_WOBATCH > 1
-  // kWB items at a time: every shared-memory read of the batch is issued
-  // before its global stores (a generic store may alias shared memory for the
-  // compiler, which would otherwise order each item's reads after the
-  // previous item's store)
+  // kWB items at a time, every shared-memory read of the batch issued before
+  // its global stores: the items' dependent read chains (gpos, sidx -> st)
+  // overlap instead of running one item after the other through the
+  // runtime-bounded loop (c4: 2 per batch -12 us, 4 -8 us, 8 +4 us)
   auto wo_items = [&](int upto) {
     constexpr int kWB = HADIS_B3_WOBATCH;
     while (wo_done < upto) {
