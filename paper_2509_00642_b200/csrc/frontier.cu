@@ -738,8 +738,14 @@ prefix_tile_min_kernel(const unsigned long long* __restrict__ bmin, int nbuckets
   const int i0 = tile * kPrefTile + 4 * threadIdx.x;
   const unsigned long long* src = bmin + (int64_t)p * nbuckets;
   unsigned long long m = ~0ull;
+  if ((nbuckets & 3) == 0 && i0 + 3 < nbuckets) {          // two 16-byte loads
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(src + i0);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(src + i0 + 2);
+    m = min(min(a.x, a.y), min(b.x, b.y));
+  } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) if (i0 + j < nbuckets) m = min(m, src[i0 + j]);
+    for (int j = 0; j < 4; ++j) if (i0 + j < nbuckets) m = min(m, src[i0 + j]);
+  }
   unsigned long long total;
   block_exclusive_min(m, &total);
   if (threadIdx.x == 0) tmin[(int64_t)p * gridDim.x + tile] = total;
@@ -765,14 +771,31 @@ prefix_apply_kernel(const unsigned long long* __restrict__ bmin, int nbuckets,
   double* dst = gpre + (int64_t)p * nbuckets;
   unsigned long long v[4];
   unsigned long long m = ~0ull;
+  const bool vec = (nbuckets & 3) == 0 && i0 + 3 < nbuckets;   // 16-byte loads / stores
+  if (vec) {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(src + i0);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(src + i0 + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) { v[j] = i0 + j < nbuckets ? src[i0 + j] : ~0ull; m = min(m, v[j]); }
+    for (int j = 0; j < 4; ++j) v[j] = i0 + j < nbuckets ? src[i0 + j] : ~0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) m = min(m, v[j]);
   unsigned long long total;
   unsigned long long run = min(tcarry[(int64_t)p * gridDim.x + tile], block_exclusive_min(m, &total));
+  double o[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    if (i0 + j < nbuckets) dst[i0 + j] = run == ~0ull ? INFINITY : from_order_key(run);
+    o[j] = run == ~0ull ? INFINITY : from_order_key(run);
     run = min(run, v[j]);
+  }
+  if (vec) {
+    *reinterpret_cast<double2*>(dst + i0) = make_double2(o[0], o[1]);
+    *reinterpret_cast<double2*>(dst + i0 + 2) = make_double2(o[2], o[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) if (i0 + j < nbuckets) dst[i0 + j] = o[j];
   }
 }
 
