@@ -37,7 +37,10 @@ namespace hadis {
 constexpr int kGuide = 4096;          // guide buckets over [0, 1]
 constexpr int kMaxBins = 2048;        // U + 1 <= kMaxBins (u16 bins)
 constexpr int kRowChunk = 32768;      // records per K1 CTA: 2^15 * 2^16 < 2^31 per limb
-constexpr int kK1Threads = 512;
+#ifndef HADIS_K1_THREADS
+#define HADIS_K1_THREADS 384   // 3 CTAs per SM (56 registers): 300 vs 308 us at 512 x 2, 256: 321, 1024: 411
+#endif
+constexpr int kK1Threads = HADIS_K1_THREADS;
 constexpr int kBkThreads = 1024;      // scatter CTA (512 x 2/SM and 4096-record tiles: slower;
 constexpr int kBkTile = 8192;         // records per scatter tile   L2 bulk prefetch ahead: slower)
 constexpr int kBkPer = kBkTile / kBkThreads;   // records per thread per tile (even)
