@@ -566,8 +566,6 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
            (4 * (lane & 7))) & 15u;
       static_assert(kRowT == 4, "class-start bits: 4 cells per lane");
       __syncwarp();
-      // one partner: S of the lane's cells, warp scan of the lane minima (the
-      // row carry enters through lane 0, so only lane 0 touches it), row test
       // the lane's cells, read from the staged window once for all partners
       // (c4: -18 us against shared-memory reads per partner)
       double2 r_hl[kRowT];
@@ -577,6 +575,8 @@ __device__ __forceinline__ void row_traverse(const Grid& g, RowSmem& sm, int p0,
         r_hl[j] = s_hl[j * kRowPad + lane];
         r_nH[j] = s_nH[j * kRowPad + lane];
       }
+      // one partner: S of the lane's cells, warp scan of the lane minima (the
+      // row carry enters through lane 0, so only lane 0 touches it), row test
       auto scan = [&](int p, double (&sv)[kRowT]) -> unsigned {
         const PairConst& pc = sm.pc[p - p0];
         const double ph = pc.ph, bh = pc.bh;
