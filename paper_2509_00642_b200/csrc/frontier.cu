@@ -1075,6 +1075,12 @@ __global__ void candidates_total_kernel(const unsigned long long* __restrict__ t
 // bucket-mates are the candidates of its segment, read straight from global
 // memory (neighbouring threads share segments, so they stay L1-resident).
 constexpr int kDecThreads = 256;
+#ifndef HADIS_DEC_CPS
+#define HADIS_DEC_CPS 32
+#endif
+#ifndef HADIS_GROUP_CPS
+#define HADIS_GROUP_CPS 4
+#endif
 
 __global__ void __launch_bounds__(kDecThreads)   // 6 / 8 CTAs per SM forced: same / worse
 decide_kernel(Grid g, const PairConst* __restrict__ pcs,
@@ -1939,11 +1945,11 @@ static int pair_frontiers(const uint32_t* pre_cnt, const uint64_t* pre_hsum, int
                             lb < 31 ? 2u << lb : 0u, (long long)hist[lb]);
   }
   // grid sizes of the two grid-stride passes measured at c4 (4 / 32 CTAs per SM)
-  group_cands_kernel<<<kNumSMs * 4, 256, 0, st>>>(g, pcs, lst, counters + 5, cand_cap, nb, (double)n, boff,
+  group_cands_kernel<<<kNumSMs * HADIS_GROUP_CPS, 256, 0, st>>>(g, pcs, lst, counters + 5, cand_cap, nb, (double)n, boff,
                                                   bcnt, grp, bmin);
   prefix(bmin, nb, tmin, gpre);                    // exact fine G for decide
   HADIS_LAUNCH_CHECK();
-  decide_kernel<<<kNumSMs * 32, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
+  decide_kernel<<<kNumSMs * HADIS_DEC_CPS, kDecThreads, 0, st>>>(g, pcs, counters, cand_cap, boff, bcnt, gpre,
                                              grp, dout);
   if (getenv("HADIS_DEBUG_BUCKETS")) {
     unsigned long long* dk = nullptr;
